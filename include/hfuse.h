@@ -1,0 +1,220 @@
+/* hfuse — B200-native horizontal kernel fusion: the C ABI (drop-in boundary).
+ *
+ * Every entry point replaces one reference (mkfuse, /root/reference/proj) interface;
+ * the citation is given per function. Conventions:
+ *   - return 0 on success, otherwise 1 + the reference ErrCode ordinal
+ *     (error.hpp:15-39: HF_E_SYNTAX = 1 ... HF_E_IO = 23) or HF_E_COMPILE / HF_E_DEVICE;
+ *   - `err` (may be NULL) receives code, 1-based source position (0 = none) and message;
+ *   - strings returned through `char**` are malloc'ed and released with hf_free();
+ *   - no function throws across the ABI; device buffers passed in are caller-owned.
+ * Thread safety: compiler entry points are reentrant (pure functions);
+ * runtime entry points act on the calling thread's current CUDA device.
+ */
+#ifndef HFUSE_H
+#define HFUSE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HF_OK = 0,
+  HF_E_SYNTAX = 1, HF_E_UNKNOWN_IDENTIFIER, HF_E_TYPE_MISMATCH, HF_E_DUPLICATE_NAME,
+  HF_E_UNRESOLVED_CALL, HF_E_UNRESOLVED_LABEL, HF_E_RECURSION, HF_E_BAD_BARRIER_ID,
+  HF_E_MISALIGNED_COUNT, HF_E_DIMENSION_MISMATCH, HF_E_GRID_MISMATCH, HF_E_THREAD_BUDGET,
+  HF_E_SHARED_OVERFLOW, HF_E_DOES_NOT_FIT, HF_E_OUT_OF_BOUNDS, HF_E_DIVIDE_BY_ZERO,
+  HF_E_BARRIER_DEADLOCK, HF_E_BARRIER_OVERFLOW, HF_E_DIVERGENT_BARRIER, HF_E_NOTHING_FEASIBLE,
+  HF_E_INCOMPATIBLE_FIXED_DIMS, HF_E_INVALID_ARGUMENT, HF_E_IO,
+  HF_E_COMPILE, HF_E_DEVICE
+};
+
+enum { HF_STYLE_STRUCTURED = 0, HF_STYLE_GOTO = 1, HF_STYLE_SM100 = 2 };
+enum { HF_REGCAP_OFF = -1, HF_REGCAP_AUTO = 0 };
+enum { HF_TIME_SINGLE = 0, HF_TIME_SEQUENTIAL = 1, HF_TIME_TWO_STREAM = 2 };
+enum { HF_BACKEND_DEVICE = 0, HF_BACKEND_COMMAND = 1 };
+
+typedef struct hf_error {
+  int code;
+  int line;
+  int col;
+  char message[512];
+} hf_error;
+
+/* fuser.hpp:24-32 BarrierEntry, plus the constituent's original id (-1 = syncthreads). */
+typedef struct hf_barrier {
+  int id;
+  int count;
+  int owner;
+  int original;
+} hf_barrier;
+
+typedef struct hf_occupancy_info {
+  int blocks_per_sm;
+  int limiting; /* 0 registers, 1 shared_memory, 2 threads, 3 block_slots */
+  int achieved_warps;
+  double occupancy_fraction;
+} hf_occupancy_info;
+
+typedef struct hf_module hf_module;
+typedef struct hf_image hf_image;
+
+typedef struct hf_module_info {
+  int threads;
+  int grid;
+  long long smem_bytes;
+  int regs;
+  int local_bytes;
+  int blocks_per_sm;
+  int n_params;
+  int n_barriers;
+} hf_module_info;
+
+typedef struct hf_timing {
+  double median_us;
+  double min_us;
+  double mean_us;
+  double max_us;
+  int reps;
+} hf_timing;
+
+/* search.hpp:11-15 EvalOutcome (device backend: cycles = median ns). */
+typedef struct hf_eval {
+  long long cycles;
+  double occupancy;
+  double utilization;
+  double us;
+  int regs;
+} hf_eval;
+
+typedef struct hf_search_opts {
+  int d0;                   /* fused block size (search_config); d0 for fixed+tunable pairs */
+  int granularity;          /* 128 in the reference sweep (search.cpp:137-138) */
+  int backend;              /* HF_BACKEND_DEVICE or HF_BACKEND_COMMAND */
+  const char* profiler_cmd; /* ExternalCommandBackend command (search.cpp:32-62) */
+  int grid;                 /* 0: the kernels' //@ grid annotation */
+  int warmup;
+  int reps;
+  int flush_l2;
+  int measured_registers;   /* r0 from ptxas register counts instead of the estimate */
+  int n_extra_caps;
+  const int* extra_caps;    /* additional register caps per partition (C4 sweep) */
+  int out_style;            /* style of *best_src */
+} hf_search_opts;
+
+typedef struct hf_device_props {
+  int sms;
+  int cc_major;
+  int cc_minor;
+  long long smem_per_sm;
+  long long smem_per_block_optin;
+  int regs_per_sm;
+  int max_threads_per_sm;
+  int clock_khz;
+  long long l2_bytes;
+  char name[128];
+} hf_device_props;
+
+void hf_free(void* p);
+const char* hf_version(void);
+
+/* ---- compiler ------------------------------------------------------------------- */
+
+/* generate_fused + emit_source (fuser.hpp:70-77), with the normalization of cmd_fuse
+ * (mkfuse.cpp:109-116: normalize_kernel(k1,"k1_") / (k2,"k2_")) and its regcap
+ * handling (mkfuse.cpp:118-133). sm_spec: "pascal-like" (default when NULL),
+ * "volta-like", "b200" or a key=value file. `table` receives up to table_cap entries. */
+int hf_fuse(const char* src1, const char* src2, int d1, int d2, int style, int regcap,
+            const char* sm_spec, char** out_src, hf_barrier* table, int table_cap,
+            int* n_entries, hf_error* err);
+
+/* The stdout report of `mkfuse fuse` (mkfuse.cpp:136-166). */
+int hf_fuse_report(const char* src1, const char* src2, int d1, int d2, int regcap,
+                   const char* sm_spec, char** out_report, hf_error* err);
+
+/* normalize_kernel (frontend.hpp:53-55) of the first kernel, printed as Mini-Kernel. */
+int hf_normalize(const char* src, const char* prefix, char** out_src, hf_error* err);
+
+/* parse_program + lint_program (frontend.hpp:13-32); report as `mkfuse check`. */
+int hf_check(const char* src, int strict, char** out_report, hf_error* err);
+
+/* MK+ (B200 dialect) -> plain Mini-Kernel with identical semantics, so the reference
+ * interpreter (exec.cpp:958-965) can execute B200 member kernels. */
+int hf_lower(const char* src, char** out_src, hf_error* err);
+
+/* sm_100a CUDA source of one unfused kernel (the baseline members). */
+int hf_emit_kernel(const char* src, int min_blocks, char** out_src, hf_error* err);
+
+/* machine.hpp:72-80 */
+int hf_register_bound(int regs1, int threads1, int regs2, int threads2, long long fused_shmem,
+                      const char* sm_spec, int* out_r0, hf_error* err);
+int hf_occupancy(int regs, long long shmem, int threads, const char* sm_spec,
+                 hf_occupancy_info* out, hf_error* err);
+
+/* ---- runtime (B200) --------------------------------------------------------------- */
+
+int hf_device_count(void);
+int hf_get_device_props(hf_device_props* out, hf_error* err);
+
+/* Fuse, emit for sm_100a and NVRTC-compile (regcap: HF_REGCAP_OFF, HF_REGCAP_AUTO = the
+ * register bound r0 of machine.cpp:269-283, or an explicit cap). grid 0 = annotation. */
+int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regcap, int grid,
+                   int min_blocks, hf_module** out, hf_error* err);
+/* One unfused kernel at its declared dims (regcap: HF_REGCAP_OFF or a cap). */
+int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks, hf_module** out,
+                    hf_error* err);
+int hf_module_get_info(const hf_module* m, hf_module_info* out);
+const char* hf_module_source(const hf_module* m);  /* borrowed */
+const char* hf_module_entry(const hf_module* m);   /* borrowed */
+int hf_module_param(const hf_module* m, int i, const char** name, int* is_array, int* is_float,
+                    int* is_written);
+int hf_module_barrier(const hf_module* m, int i, hf_barrier* out);
+int hf_module_cubin(const hf_module* m, const void** data, size_t* size);
+/* Raw launch: args[i] points at the i-th parameter value (device pointer or scalar). */
+int hf_launch(const hf_module* m, int grid, void** args, void* stream, hf_error* err);
+void hf_module_free(hf_module* m);
+
+/* MemoryImage (memimage.hpp:36-68); seeded arrays are generated in HBM on upload. */
+int hf_image_parse(const char* text, int has_seed, unsigned long long seed, hf_image** out,
+                   hf_error* err);
+int hf_image_merge(hf_image* dst, hf_image* src, hf_error* err); /* consumes src's entries */
+int hf_image_materialize(hf_image* img, hf_error* err);         /* host-side generation */
+int hf_image_upload(hf_image* img, void* stream, hf_error* err);
+int hf_image_download(hf_image* img, void* stream, hf_error* err);
+int hf_image_digest(const hf_image* img, unsigned long long* out, hf_error* err);
+int hf_image_serialize(const hf_image* img, char** out, hf_error* err);
+int hf_image_count(const hf_image* img);
+int hf_image_entry(hf_image* img, int i, const char** name, void** dev_ptr, int32_t** host_ptr,
+                   long long* len, int* is_float);
+int hf_image_find(hf_image* img, const char* name, void** dev_ptr, int32_t** host_ptr,
+                  long long* len, int* is_float);
+int hf_image_set_host(hf_image* img, const char* name, const void* data, long long len,
+                      hf_error* err); /* replace an array's contents with host data */
+long long hf_image_bytes(const hf_image* img);
+void hf_image_free(hf_image* img);
+
+/* run_functional (sim.hpp:43-52) on the device: bind parameters by name and launch. */
+int hf_run(const hf_module* m, hf_image* img, int grid, void* stream, hf_error* err);
+
+/* Device timing with CUDA events (replaces run_timed, exec.cpp:967-982). */
+int hf_time(int mode, const hf_module* a, const hf_module* b, hf_image* img, int grid_a,
+            int grid_b, int warmup, int reps, int flush_l2, void* stream, hf_timing* out,
+            hf_error* err);
+
+/* ProfilerBackend::evaluate (search.hpp:19-23) for one candidate on the device. */
+int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, hf_image* img,
+               int grid, int warmup, int reps, int flush_l2, hf_eval* out, hf_error* err);
+
+/* search_config / fixed_partition_fuse + trace_csv (search.hpp:66-77). img may be NULL for
+ * the command backend. */
+int hf_search(const char* src1, const char* src2, hf_image* img, const hf_search_opts* opts,
+              int* best_d1, int* best_d2, int* best_regcap, long long* best_time,
+              char** trace_csv, char** best_src, hf_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HFUSE_H */

@@ -1,0 +1,103 @@
+#include "driver.hpp"
+
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+
+namespace hf {
+
+std::string read_text(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) raise(Code::Io, "cannot open '" + path + "'");
+  std::stringstream ss;
+  ss << in.rdbuf();
+  return ss.str();
+}
+
+Loaded load_source(const std::string& src, const std::string& entry, Dialect dialect) {
+  Loaded l;
+  l.prog = parse(src, dialect);
+  if (l.prog.kernels.empty()) raise(Code::InvalidArgument, "source defines no kernel");
+  if (entry.empty()) {
+    l.kernel = l.prog.kernels.front();
+  } else {
+    const Kernel* k = l.prog.kernel(entry);
+    if (!k) raise(Code::InvalidArgument, "source has no kernel '" + entry + "'");
+    l.kernel = *k;
+  }
+  return l;
+}
+
+FuseResult fuse_sources(const std::string& src1, const std::string& src2, int d1, int d2,
+                        const std::string& regcap, const SM& sm) {
+  FuseResult r;
+  r.sm = sm;
+  Loaded k1 = load_source(src1), k2 = load_source(src2);
+  r.n1 = normalize(k1.kernel, k1.prog.funcs, "k1_");
+  r.n2 = normalize(k2.kernel, k2.prog.funcs, "k2_");
+  r.fused = fuse(r.n1, r.n2, d1, d2, sm);
+  r.r1 = resources_of(r.n1, d1);
+  r.r2 = resources_of(r.n2, d2);
+  r.rf = resources_of(r.fused.to_kernel(), r.fused.cfg.d0);
+  try {
+    r.r0 = register_bound(r.r1, r.r2, r.rf.shmem, r.fused.cfg.d0, sm);
+  } catch (const Error&) {
+    r.r0 = -1;
+  }
+  if (regcap == "auto") {
+    if (r.r0 > 0) r.fused.cfg.reg_cap = r.r0;
+  } else if (regcap != "off") {
+    int v = std::stoi(regcap);
+    if (v <= 0) raise(Code::InvalidArgument, "register cap must be positive");
+    r.fused.cfg.reg_cap = v;
+  }
+  return r;
+}
+
+std::string fuse_report(const FuseResult& r) {
+  const Fused& f = r.fused;
+  std::string o;
+  char buf[256];
+  o += "fused_kernel = " + f.name + "\n";
+  std::snprintf(buf, sizeof(buf), "partition = d1 %d (%s), d2 %d (%s), d0 %d\n", f.cfg.d1, f.k1_name.c_str(),
+                f.cfg.d2, f.k2_name.c_str(), f.cfg.d0);
+  o += buf;
+  for (const auto& e : f.barriers) {
+    int uses = 0;
+    walk(e.owner == 1 ? f.body1 : f.body2, [&](const Stmt& s) {
+      if (s.k == SK::BarSync && s.bid == e.id) ++uses;
+    });
+    std::snprintf(buf, sizeof(buf), "barrier id %d: count %d, constituent %d, uses %d\n", e.id, e.count, e.owner,
+                  uses);
+    o += buf;
+  }
+  std::snprintf(buf, sizeof(buf), "registers = k1 %d, k2 %d, fused %d\n", r.r1.regs, r.r2.regs, r.rf.regs);
+  o += buf;
+  o += "shared_bytes = " + std::to_string(r.rf.shmem) + "\n";
+  if (f.cfg.reg_cap) o += "reg_cap = " + std::to_string(*f.cfg.reg_cap) + "\n";
+  else if (r.r0 > 0) o += "suggested_reg_cap = " + std::to_string(r.r0) + "\n";
+  Resources capped = r.rf;
+  if (f.cfg.reg_cap) capped.regs = std::min(capped.regs, *f.cfg.reg_cap);
+  Occupancy occ = occupancy(capped, r.sm);
+  o += "blocks_per_sm = " + std::to_string(occ.blocks_per_sm) + "\n";
+  o += std::string("limiting_resource = ") + limit_name(occ.limiting) + "\n";
+  o += "achieved_warps = " + std::to_string(occ.warps) + "\n";
+  std::snprintf(buf, sizeof(buf), "occupancy_fraction = %.6f\n", occ.fraction);
+  o += buf;
+  return o;
+}
+
+std::string emit(const Fused& f, Style style) {
+  switch (style) {
+    case Style::Structured: return emit_structured(f);
+    case Style::Goto: return emit_goto(f);
+    case Style::Sm100: {
+      std::string s = emit_sm100(f).source;
+      if (f.cfg.reg_cap) s = "// hfuse: compile with --maxrregcount=" + std::to_string(*f.cfg.reg_cap) + "\n" + s;
+      return s;
+    }
+  }
+  return {};
+}
+
+}  // namespace hf

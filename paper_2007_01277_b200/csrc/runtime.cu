@@ -1,0 +1,382 @@
+// Device runtime for hfuse on B200 (sm_100a). See runtime.hpp.
+//
+// * NVRTC compiles emitted kernels straight to an sm_100a CUBIN (no PTX JIT at load).
+// * Driver entry points come from cudaGetDriverEntryPoint so this library links only the
+//   static CUDA runtime + NVRTC and still loads on hosts without libcuda (CPU CI).
+// * Memory images live in HBM; seeded arrays are generated on the device with the
+//   closed form of the reference's splitmix64 stream (memimage.cpp:10-61): element i of
+//   a seeded array is mix(seed + (i + 1) * golden), so every thread fills independently
+//   and the result is bit-identical to the CPU generator.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+
+#include "runtime.hpp"
+
+namespace hf::rt {
+namespace {
+
+#define HF_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      raise(Code::Device, std::string(#call) + ": " + cudaGetErrorString(e_));                \
+  } while (0)
+
+struct Driver {
+  CUresult (*moduleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*moduleUnload)(CUmodule) = nullptr;
+  CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           unsigned, CUstream, void**, void**) = nullptr;
+  CUresult (*funcGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
+  CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
+  CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+};
+
+template <typename F>
+void resolve(const char* sym, F& fp) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+#pragma nv_diag_suppress 1444
+  cudaError_t e = cudaGetDriverEntryPoint(sym, &p, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p)
+    raise(Code::Device, std::string("driver entry point unavailable: ") + sym);
+  fp = reinterpret_cast<F>(p);
+}
+
+Driver& drv() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    HF_CUDA(cudaFree(nullptr));  // create the primary context
+    resolve("cuModuleLoadData", d.moduleLoadData);
+    resolve("cuModuleGetFunction", d.moduleGetFunction);
+    resolve("cuModuleUnload", d.moduleUnload);
+    resolve("cuLaunchKernel", d.launchKernel);
+    resolve("cuFuncGetAttribute", d.funcGetAttribute);
+    resolve("cuFuncSetAttribute", d.funcSetAttribute);
+    resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy);
+    resolve("cuGetErrorString", d.getErrorString);
+  });
+  return d;
+}
+
+void cu_check(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return;
+  const char* s = "unknown";
+  if (drv().getErrorString) drv().getErrorString(r, &s);
+  raise(Code::Device, std::string(what) + ": " + s);
+}
+
+__device__ __forceinline__ unsigned long long sm64_mix(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_uniform(float* __restrict__ out, long long n, unsigned long long seed, float lo,
+                             float hi) {
+  const float span = __fsub_rn(hi, lo);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long bits = sm64_mix(seed + (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ULL);
+    float unit = __fmul_rn((float)(bits >> 40), 1.0f / 16777216.0f);
+    out[i] = __fadd_rn(lo, __fmul_rn(unit, span));
+  }
+}
+
+__global__ void fill_range(int* __restrict__ out, long long n, unsigned long long seed, int lo,
+                           unsigned long long span) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long bits = sm64_mix(seed + (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ULL);
+    out[i] = (int)(lo + (long long)(bits % span));
+  }
+}
+
+int fill_grid(int64_t n) {
+  int64_t blocks = (n + 255) / 256;
+  return int(std::min<int64_t>(blocks, 148 * 16));
+}
+
+void* g_flush = nullptr;
+size_t g_flush_bytes = 0;
+
+void flush_l2(cudaStream_t s) {
+  if (!g_flush) {
+    g_flush_bytes = size_t(512) << 20;  // 4x the 126 MB L2
+    HF_CUDA(cudaMalloc(&g_flush, g_flush_bytes));
+  }
+  static int salt = 0;
+  HF_CUDA(cudaMemsetAsync(g_flush, (++salt) & 0xff, g_flush_bytes, s));
+}
+
+}  // namespace
+
+bool device_available() {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
+Props props(int device) {
+  if (device < 0) HF_CUDA(cudaGetDevice(&device));
+  cudaDeviceProp p;
+  HF_CUDA(cudaGetDeviceProperties(&p, device));
+  Props r;
+  r.device = device;
+  r.sms = p.multiProcessorCount;
+  r.cc_major = p.major;
+  r.cc_minor = p.minor;
+  r.smem_per_sm = int64_t(p.sharedMemPerMultiprocessor);
+  r.smem_per_block_optin = int64_t(p.sharedMemPerBlockOptin);
+  r.regs_per_sm = p.regsPerMultiprocessor;
+  r.max_threads_per_sm = p.maxThreadsPerMultiProcessor;
+  r.max_threads_per_block = p.maxThreadsPerBlock;
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+  r.clock_khz = clk;
+  r.l2_bytes = p.l2CacheSize;
+  r.name = p.name;
+  return r;
+}
+
+SM sm_from_device(int device) {
+  Props p = props(device);
+  SM sm = SM::b200();
+  sm.num_sms = p.sms;
+  sm.regs_per_sm = p.regs_per_sm;
+  sm.shmem_per_sm = p.smem_per_sm;
+  sm.max_shmem_per_block = p.smem_per_block_optin;
+  sm.max_threads_per_sm = p.max_threads_per_sm;
+  sm.max_threads_per_block = p.max_threads_per_block;
+  return sm;
+}
+
+Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) {
+  Module m;
+  m.entry = k.entry;
+  m.source = k.source;
+  m.threads = k.threads;
+  m.grid = k.grid;
+  m.smem = k.smem_bytes;
+  m.params = k.params;
+  m.barriers = k.barriers;
+  m.maxrreg = maxrreg;
+
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, k.source.c_str(), (k.entry + ".cu").c_str(), 0, nullptr, nullptr) !=
+      NVRTC_SUCCESS)
+    raise(Code::Compile, "nvrtcCreateProgram failed");
+  std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-fmad=false"};
+  if (lineinfo) opts.push_back("-lineinfo");
+  if (maxrreg) opts.push_back("--maxrregcount=" + std::to_string(*maxrreg));
+  std::vector<const char*> argv;
+  for (const auto& o : opts) argv.push_back(o.c_str());
+  nvrtcResult r = nvrtcCompileProgram(prog, int(argv.size()), argv.data());
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  m.log.resize(log_size);
+  if (log_size) nvrtcGetProgramLog(prog, m.log.data());
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    raise(Code::Compile, "NVRTC failed for '" + k.entry + "': " + m.log);
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  m.cubin.resize(n);
+  nvrtcGetCUBIN(prog, m.cubin.data());
+  nvrtcDestroyProgram(&prog);
+
+  if (!device_available()) return m;  // CPU hosts: compile-only (ptxas still ran)
+  Driver& d = drv();
+  HF_CUDA(cudaGetDevice(&m.device));
+  CUmodule mod;
+  cu_check(d.moduleLoadData(&mod, m.cubin.data()), "cuModuleLoadData");
+  CUfunction fn;
+  cu_check(d.moduleGetFunction(&fn, mod, k.entry.c_str()), "cuModuleGetFunction");
+  m.mod = mod;
+  m.fn = fn;
+  if (m.smem > 48 * 1024)
+    cu_check(d.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, int(m.smem)),
+             "cuFuncSetAttribute(max dynamic smem)");
+  cu_check(d.funcGetAttribute(&m.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, fn), "cuFuncGetAttribute");
+  cu_check(d.funcGetAttribute(&m.local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, fn), "cuFuncGetAttribute");
+  cu_check(d.occupancy(&m.blocks_per_sm, fn, m.threads, size_t(m.smem)), "cuOccupancyMaxActiveBlocks");
+  return m;
+}
+
+void unload(Module& m) {
+  if (m.mod) drv().moduleUnload(static_cast<CUmodule>(m.mod));
+  m.mod = m.fn = nullptr;
+}
+
+void upload(Image& img, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HF_CUDA(cudaGetDevice(&img.device));
+  for (auto& [name, a] : img.arrays) {
+    if (!a.dev) HF_CUDA(cudaMalloc(&a.dev, size_t(a.len) * 4));
+    switch (a.mode) {
+      case ArrayEntry::Mode::Zero:
+        if (a.host_valid) HF_CUDA(cudaMemcpyAsync(a.dev, a.host.data(), size_t(a.len) * 4, cudaMemcpyHostToDevice, s));
+        else HF_CUDA(cudaMemsetAsync(a.dev, 0, size_t(a.len) * 4, s));
+        break;
+      case ArrayEntry::Mode::Values:
+        HF_CUDA(cudaMemcpyAsync(a.dev, a.host.data(), size_t(a.len) * 4, cudaMemcpyHostToDevice, s));
+        break;
+      case ArrayEntry::Mode::SeedUniform:
+        fill_uniform<<<fill_grid(a.len), 256, 0, s>>>(static_cast<float*>(a.dev), a.len, a.seed, a.flo, a.fhi);
+        HF_CUDA(cudaGetLastError());
+        break;
+      case ArrayEntry::Mode::SeedRange: {
+        unsigned long long span = (unsigned long long)(int64_t(a.ihi) - a.ilo) + 1;
+        fill_range<<<fill_grid(a.len), 256, 0, s>>>(static_cast<int*>(a.dev), a.len, a.seed, a.ilo, span);
+        HF_CUDA(cudaGetLastError());
+        break;
+      }
+    }
+    a.dev_valid = true;
+  }
+  HF_CUDA(cudaStreamSynchronize(s));
+}
+
+void download(Image& img, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (auto& [name, a] : img.arrays) {
+    if (!a.dev_valid) raise(Code::InvalidArgument, "array '" + name + "' is not on the device");
+    a.host.resize(size_t(a.len));
+    HF_CUDA(cudaMemcpyAsync(a.host.data(), a.dev, size_t(a.len) * 4, cudaMemcpyDeviceToHost, s));
+    a.host_valid = true;
+  }
+  HF_CUDA(cudaStreamSynchronize(s));
+}
+
+void release(Image& img) {
+  for (auto& [name, a] : img.arrays) {
+    if (a.dev) cudaFree(a.dev);
+    a.dev = nullptr;
+    a.dev_valid = false;
+  }
+}
+
+void* device_ptr(Image& img, const std::string& name) {
+  auto it = img.arrays.find(name);
+  if (it == img.arrays.end() || !it->second.dev)
+    raise(Code::InvalidArgument, "memory image does not provide array '" + name + "'");
+  return it->second.dev;
+}
+
+void launch_raw(const Module& m, int grid, void** args, void* stream) {
+  if (!m.fn) raise(Code::Device, "module '" + m.entry + "' is not loaded (no GPU?)");
+  cu_check(drv().launchKernel(static_cast<CUfunction>(m.fn), unsigned(grid), 1, 1, unsigned(m.threads), 1, 1,
+                              unsigned(m.smem), static_cast<CUstream>(stream), args, nullptr),
+           "cuLaunchKernel");
+}
+
+namespace {
+struct Bound {
+  std::vector<void*> ptrs;
+  std::vector<int32_t> cells;
+  std::vector<void*> args;
+};
+
+Bound bind(const Module& m, Image& img) {
+  Bound b;
+  b.ptrs.resize(m.params.size());
+  b.cells.resize(m.params.size());
+  b.args.resize(m.params.size());
+  for (size_t i = 0; i < m.params.size(); ++i) {
+    const Sm100Param& p = m.params[i];
+    if (p.array) {
+      auto it = img.arrays.find(p.name);
+      if (it == img.arrays.end())
+        raise(Code::InvalidArgument, "memory image does not provide array '" + p.name + "'");
+      if (it->second.ty != p.ty) raise(Code::TypeMismatch, "array '" + p.name + "' element type mismatch");
+      if (!it->second.dev_valid) raise(Code::InvalidArgument, "array '" + p.name + "' is not on the device");
+      b.ptrs[i] = it->second.dev;
+      b.args[i] = &b.ptrs[i];
+    } else {
+      auto it = img.scalars.find(p.name);
+      if (it == img.scalars.end())
+        raise(Code::InvalidArgument, "memory image does not provide scalar '" + p.name + "'");
+      if (it->second.ty != p.ty) raise(Code::TypeMismatch, "scalar '" + p.name + "' type mismatch");
+      if (p.ty == Ty::Int) b.cells[i] = it->second.i;
+      else std::memcpy(&b.cells[i], &it->second.f, 4);
+      b.args[i] = &b.cells[i];
+    }
+  }
+  return b;
+}
+}  // namespace
+
+void launch(const Module& m, Image& img, int grid, void* stream) {
+  Bound b = bind(m, img);
+  launch_raw(m, grid > 0 ? grid : m.grid, b.args.data(), stream);
+}
+
+Timing time(Mode mode, const Module& a, const Module* b, Image& img, int grid_a, int grid_b, int warmup, int reps,
+            bool flush, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (mode != Mode::Single && !b) raise(Code::InvalidArgument, "pair timing needs two modules");
+  Bound ba = bind(a, img);
+  Bound bb;
+  if (b) bb = bind(*b, img);
+  int ga = grid_a > 0 ? grid_a : a.grid;
+  int gb = b ? (grid_b > 0 ? grid_b : b->grid) : 0;
+  cudaStream_t s2 = nullptr;
+  if (mode == Mode::TwoStream) HF_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1, ej;
+  HF_CUDA(cudaEventCreate(&e0));
+  HF_CUDA(cudaEventCreate(&e1));
+  HF_CUDA(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+  auto run_once = [&]() {
+    HF_CUDA(cudaEventRecord(e0, s));
+    if (mode == Mode::Single) {
+      launch_raw(a, ga, ba.args.data(), s);
+    } else if (mode == Mode::Sequential) {
+      launch_raw(a, ga, ba.args.data(), s);
+      launch_raw(*b, gb, bb.args.data(), s);
+    } else {
+      HF_CUDA(cudaStreamWaitEvent(s2, e0, 0));
+      launch_raw(a, ga, ba.args.data(), s);
+      launch_raw(*b, gb, bb.args.data(), s2);
+      HF_CUDA(cudaEventRecord(ej, s2));
+      HF_CUDA(cudaStreamWaitEvent(s, ej, 0));
+    }
+    HF_CUDA(cudaEventRecord(e1, s));
+  };
+  for (int i = 0; i < warmup; ++i) run_once();
+  std::vector<double> us;
+  for (int i = 0; i < reps; ++i) {
+    if (flush) flush_l2(s);
+    run_once();
+    HF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    HF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    us.push_back(double(ms) * 1000.0);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(ej);
+  if (s2) cudaStreamDestroy(s2);
+  Timing t;
+  t.reps = reps;
+  if (us.empty()) return t;
+  std::vector<double> sorted = us;
+  std::sort(sorted.begin(), sorted.end());
+  t.median_us = sorted[sorted.size() / 2];
+  t.min_us = sorted.front();
+  t.max_us = sorted.back();
+  t.mean_us = std::accumulate(us.begin(), us.end(), 0.0) / double(us.size());
+  return t;
+}
+
+void synchronize() { HF_CUDA(cudaDeviceSynchronize()); }
+
+}  // namespace hf::rt

@@ -1,0 +1,75 @@
+// Device runtime: NVRTC compilation for sm_100a, module load/launch through the CUDA
+// driver API (entry points resolved from the static runtime, so the library loads on
+// GPU-less hosts), memory images in HBM, and CUDA-event timing (the device profiler that
+// replaces the reference's cycle simulator, /root/reference/proj/src/exec.cpp:144-167).
+#pragma once
+
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "fuser.hpp"
+#include "image.hpp"
+
+namespace hf::rt {
+
+struct Module {
+  std::string entry;
+  std::string source;
+  int threads = 0;
+  int grid = 1;
+  int64_t smem = 0;
+  std::vector<Sm100Param> params;
+  std::vector<BarrierEntry> barriers;
+  std::optional<int> maxrreg;
+  // filled after load
+  int regs = 0;
+  int local_bytes = 0;  // spill / local memory per thread
+  int blocks_per_sm = 0;
+  std::string log;
+  std::vector<char> cubin;
+  void* mod = nullptr;
+  void* fn = nullptr;
+  int device = 0;
+};
+
+struct Props {
+  int device = 0;
+  int sms = 0;
+  int cc_major = 0, cc_minor = 0;
+  int64_t smem_per_sm = 0, smem_per_block_optin = 0;
+  int regs_per_sm = 0, max_threads_per_sm = 0, max_threads_per_block = 0;
+  int clock_khz = 0;
+  int64_t l2_bytes = 0;
+  std::string name;
+};
+
+Props props(int device = -1);
+SM sm_from_device(int device = -1);
+bool device_available();
+
+Module compile(const Sm100Kernel& k, std::optional<int> maxrreg = std::nullopt, bool lineinfo = true);
+void unload(Module& m);
+
+void upload(Image& img, void* stream = nullptr);
+void download(Image& img, void* stream = nullptr);
+void release(Image& img);
+void* device_ptr(Image& img, const std::string& name);
+
+// Binds parameters by name from the image (exec.cpp:190-216) and launches.
+void launch(const Module& m, Image& img, int grid, void* stream = nullptr);
+void launch_raw(const Module& m, int grid, void** args, void* stream = nullptr);
+
+struct Timing {
+  double median_us = 0, min_us = 0, mean_us = 0, max_us = 0;
+  int reps = 0;
+};
+enum class Mode { Single, Sequential, TwoStream };
+// Times `a` (Single) or the pair a;b (Sequential) / a||b on two streams (TwoStream).
+// L2 is flushed before every timed repetition when `flush_l2`.
+Timing time(Mode mode, const Module& a, const Module* b, Image& img, int grid_a, int grid_b, int warmup,
+            int reps, bool flush_l2, void* stream = nullptr);
+
+void synchronize();
+
+}  // namespace hf::rt

@@ -1,0 +1,84 @@
+// Profile-guided partition search (Algorithm "Main").
+// Reference contract: /root/reference/proj/include/mkfuse/search.hpp:11-77 — same sweep
+// (d1 = g, 2g, ..., d0 - g; uncapped then capped at r0), same strict-< fold (ties keep the
+// smaller d1, then no cap), infeasible candidates skipped, NothingFeasible when none.
+// The B200 backend (DeviceBackend) times each candidate on the GPU instead of simulating.
+#pragma once
+
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "fuser.hpp"
+#include "image.hpp"
+
+namespace hf {
+
+struct EvalOutcome {
+  int64_t cycles = 0;        // device backend: nanoseconds (median)
+  double occupancy = 0.0;
+  double utilization = 0.0;
+  double us = 0.0;           // device backend: median microseconds
+  int regs = 0;
+};
+
+class ProfilerBackend {
+ public:
+  virtual ~ProfilerBackend() = default;
+  virtual EvalOutcome evaluate(const Fused& fused, const FusionConfig& cfg) = 0;
+  // Per-thread resources of one constituent run alone with `threads` threads; the
+  // default is the reference's estimate (machine.cpp:215-230).
+  virtual Resources resources(const Kernel& k, int threads) { return resources_of(k, threads); }
+};
+
+// Spawns `command <source-file>` and reads the first integer of its stdout (search.cpp:32-62).
+class ExternalCommandBackend : public ProfilerBackend {
+ public:
+  explicit ExternalCommandBackend(std::string cmd, Style style = Style::Goto);
+  EvalOutcome evaluate(const Fused& fused, const FusionConfig& cfg) override;
+
+ private:
+  std::string cmd_;
+  Style style_;
+  int counter_ = 0;
+};
+
+// Times the sm_100a emission of every candidate on the current GPU.
+class DeviceBackend : public ProfilerBackend {
+ public:
+  DeviceBackend(Image& img, int grid, int warmup = 3, int reps = 10, bool flush_l2 = true,
+                bool measured_registers = true);
+  EvalOutcome evaluate(const Fused& fused, const FusionConfig& cfg) override;
+  Resources resources(const Kernel& k, int threads) override;
+
+ private:
+  Image& img_;
+  int grid_, warmup_, reps_;
+  bool flush_, measured_;
+};
+
+struct EvalPoint {
+  FusionConfig cfg;
+  EvalOutcome out;
+};
+
+struct SearchResult {
+  Fused best;
+  FusionConfig best_cfg;
+  int64_t best_time = 0;
+  std::vector<EvalPoint> trace;
+};
+
+struct SearchOptions {
+  int granularity = 128;
+  std::vector<int> extra_caps;  // C4: additional register caps evaluated per partition
+};
+
+SearchResult search_config(const Kernel& k1, const Kernel& k2, int d0, ProfilerBackend& be, const SM& sm,
+                           const SearchOptions& opt = {});
+SearchResult fixed_partition_fuse(const Kernel& k1, const Kernel& k2, ProfilerBackend& be, const SM& sm,
+                                  int d0 = 1024, const SearchOptions& opt = {});
+std::string trace_csv(const SearchResult& r);
+
+}  // namespace hf
