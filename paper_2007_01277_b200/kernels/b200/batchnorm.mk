@@ -1,0 +1,165 @@
+// BatchNorm collect-statistics, B200 form (MK+).
+// Semantics of PyTorch's batch_norm_collect_statistics (PAPER.md:274-325, the corpus
+// analogue /root/reference/proj/corpus/batchnorm.mk): per channel c of x[N, C, HW] the
+// mean and the biased variance, via Welford updates merged with Chan's formula.
+// B200 mechanics: each channel's N planes are walked as one flat float4 index space
+// (128-bit coalesced loads, HW % 4 == 0), one Chan merge per float4 instead of one
+// division per element, a 5-step warp-shuffle tree and a shared-memory stage per warp.
+// Grid-stride over channels, so any common grid works.
+//@ grid=256
+kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) dims (1024, 1, 1) {
+  shared int bn_sn[32];
+  shared float bn_savg[32];
+  shared float bn_sm2[32];
+  int tid = threadIdx.x;
+  int nthr = blockDim.x * blockDim.y * blockDim.z;
+  int hw4 = bn_HW / 4;
+  int lane = tid % 32;
+  int warp = tid / 32;
+  int nwarps = nthr / 32;
+  float v0; float v1; float v2; float v3;
+  float avg; float m2; int n; float o_avg; float o_m2; int o_n; int tot; float fac; float delta;
+  for (int c = blockIdx.x; c < bn_C; c = c + gridDim.x) {
+    avg = 0.0;
+    m2 = 0.0;
+    n = 0;
+    int b = 0;
+    int i = tid;
+    while (i >= hw4) {
+      i = i - hw4;
+      b = b + 1;
+    }
+    while (b < bn_N) {
+      vload(bn_x, (b * bn_C + c) * hw4 + i, v0, v1, v2, v3);
+      float m4 = ((v0 + v1) + (v2 + v3)) * 0.25;
+      float d0 = v0 - m4;
+      float d1 = v1 - m4;
+      float d2 = v2 - m4;
+      float d3 = v3 - m4;
+      float q = (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+      tot = n + 4;
+      delta = m4 - avg;
+      fac = 1.0 / tot;
+      avg = avg + delta * 4.0 * fac;
+      m2 = m2 + q + delta * delta * n * 4.0 * fac;
+      n = tot;
+      i = i + nthr;
+      while (i >= hw4) {
+        i = i - hw4;
+        b = b + 1;
+      }
+    }
+    o_n = warp_shfl_xor(n, 16);
+    o_avg = warp_shfl_xor(avg, 16);
+    o_m2 = warp_shfl_xor(m2, 16);
+    tot = n + o_n;
+    fac = 1.0 / fmaxf(1.0, tot);
+    delta = o_avg - avg;
+    m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+    avg = (n * avg + o_n * o_avg) * fac;
+    n = tot;
+    o_n = warp_shfl_xor(n, 8);
+    o_avg = warp_shfl_xor(avg, 8);
+    o_m2 = warp_shfl_xor(m2, 8);
+    tot = n + o_n;
+    fac = 1.0 / fmaxf(1.0, tot);
+    delta = o_avg - avg;
+    m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+    avg = (n * avg + o_n * o_avg) * fac;
+    n = tot;
+    o_n = warp_shfl_xor(n, 4);
+    o_avg = warp_shfl_xor(avg, 4);
+    o_m2 = warp_shfl_xor(m2, 4);
+    tot = n + o_n;
+    fac = 1.0 / fmaxf(1.0, tot);
+    delta = o_avg - avg;
+    m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+    avg = (n * avg + o_n * o_avg) * fac;
+    n = tot;
+    o_n = warp_shfl_xor(n, 2);
+    o_avg = warp_shfl_xor(avg, 2);
+    o_m2 = warp_shfl_xor(m2, 2);
+    tot = n + o_n;
+    fac = 1.0 / fmaxf(1.0, tot);
+    delta = o_avg - avg;
+    m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+    avg = (n * avg + o_n * o_avg) * fac;
+    n = tot;
+    o_n = warp_shfl_xor(n, 1);
+    o_avg = warp_shfl_xor(avg, 1);
+    o_m2 = warp_shfl_xor(m2, 1);
+    tot = n + o_n;
+    fac = 1.0 / fmaxf(1.0, tot);
+    delta = o_avg - avg;
+    m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+    avg = (n * avg + o_n * o_avg) * fac;
+    n = tot;
+    if (lane == 0) {
+      bn_sn[warp] = n;
+      bn_savg[warp] = avg;
+      bn_sm2[warp] = m2;
+    }
+    syncthreads();
+    if (warp == 0) {
+      if (lane < nwarps) {
+        n = bn_sn[lane];
+        avg = bn_savg[lane];
+        m2 = bn_sm2[lane];
+      } else {
+        n = 0;
+        avg = 0.0;
+        m2 = 0.0;
+      }
+      o_n = warp_shfl_xor(n, 16);
+      o_avg = warp_shfl_xor(avg, 16);
+      o_m2 = warp_shfl_xor(m2, 16);
+      tot = n + o_n;
+      fac = 1.0 / fmaxf(1.0, tot);
+      delta = o_avg - avg;
+      m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+      avg = (n * avg + o_n * o_avg) * fac;
+      n = tot;
+      o_n = warp_shfl_xor(n, 8);
+      o_avg = warp_shfl_xor(avg, 8);
+      o_m2 = warp_shfl_xor(m2, 8);
+      tot = n + o_n;
+      fac = 1.0 / fmaxf(1.0, tot);
+      delta = o_avg - avg;
+      m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+      avg = (n * avg + o_n * o_avg) * fac;
+      n = tot;
+      o_n = warp_shfl_xor(n, 4);
+      o_avg = warp_shfl_xor(avg, 4);
+      o_m2 = warp_shfl_xor(m2, 4);
+      tot = n + o_n;
+      fac = 1.0 / fmaxf(1.0, tot);
+      delta = o_avg - avg;
+      m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+      avg = (n * avg + o_n * o_avg) * fac;
+      n = tot;
+      o_n = warp_shfl_xor(n, 2);
+      o_avg = warp_shfl_xor(avg, 2);
+      o_m2 = warp_shfl_xor(m2, 2);
+      tot = n + o_n;
+      fac = 1.0 / fmaxf(1.0, tot);
+      delta = o_avg - avg;
+      m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+      avg = (n * avg + o_n * o_avg) * fac;
+      n = tot;
+      o_n = warp_shfl_xor(n, 1);
+      o_avg = warp_shfl_xor(avg, 1);
+      o_m2 = warp_shfl_xor(m2, 1);
+      tot = n + o_n;
+      fac = 1.0 / fmaxf(1.0, tot);
+      delta = o_avg - avg;
+      m2 = m2 + o_m2 + delta * delta * n * o_n * fac;
+      avg = (n * avg + o_n * o_avg) * fac;
+      n = tot;
+      if (lane == 0) {
+        bn_stats[c * 2] = avg;
+        bn_stats[c * 2 + 1] = m2 / fmaxf(1.0, n);
+      }
+    }
+    syncthreads();
+  }
+}

@@ -1,0 +1,69 @@
+"""Catalog of the DL member kernels and their synthetic workloads.
+
+Each member has two Mini-Kernel sources under kernels/: `ref/` — the naive form a user
+would write (the input of the naive goto fusion and the semantic reference) — and `b200/`
+— the MK+ form with the Blackwell mechanics the fused hot path uses. Images are
+memory-image texts (memimage.cpp format) whose seeded arrays are generated in HBM.
+`bytes` is the algorithmic HBM traffic of one launch (the roofline numerator).
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Callable, Dict
+
+KERNELS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "kernels")
+
+
+def source(form: str, stem: str) -> str:
+    with open(os.path.join(KERNELS, form, stem + ".mk")) as f:
+        return f.read()
+
+
+@dataclass
+class Workload:
+    image: str        # memory-image text
+    bytes: int        # algorithmic bytes per launch (reads + writes)
+    desc: str
+
+
+@dataclass
+class Member:
+    key: str
+    stem: str
+    sizes: Dict[str, Callable[[int], Workload]]  # size name -> f(seed offset) -> Workload
+
+
+def _bn(N: int, C: int, HW: int) -> Callable[[int], Workload]:
+    def make(seed: int = 0) -> Workload:
+        n = N * C * HW
+        img = (f"array bn_x float32 {n} seed {1 + seed} uniform -1 1\n"
+               f"array bn_stats float32 {2 * C} zero\n"
+               f"scalar bn_N int32 {N}\nscalar bn_C int32 {C}\nscalar bn_HW int32 {HW}\n")
+        return Workload(img, 4 * n + 8 * C, f"bn_stats x[{N},{C},{HW}] fp32")
+    return make
+
+
+def _hist(n: int, lo: float = -4.0, hi: float = 4.0) -> Callable[[int], Workload]:
+    def make(seed: int = 0) -> Workload:
+        img = (f"array hi_x float32 {n} seed {2 + seed} uniform {lo:g} {hi:g}\n"
+               f"array hi_out int32 64 zero\nscalar hi_n int32 {n}\n")
+        return Workload(img, 4 * n + 4 * 64, f"hist 64 bins over [-4,4], {n} fp32")
+    return make
+
+
+MEMBERS: Dict[str, Member] = {
+    "bn": Member("bn", "batchnorm", {
+        "full": _bn(64, 256, 56 * 56),
+        "parity": _bn(2, 8, 56 * 56),
+        "tiny": _bn(1, 3, 16),
+    }),
+    "hist": Member("hist", "histogram", {
+        "full": _hist(64 * 256 * 56 * 56),
+        "parity": _hist(2 * 8 * 56 * 56, -4.5, 4.5),
+        "tiny": _hist(64, -5.0, 5.0),
+    }),
+}
+
+# The ten DL pairs of the paper, over the members built so far.
+PAIRS = [("bn", "hist")]
