@@ -3,8 +3,9 @@
 // analogue /root/reference/proj/corpus/batchnorm.mk): per channel c of x[N, C, HW] the
 // mean and the biased variance, via Welford updates merged with Chan's formula.
 // B200 mechanics: each channel's N planes are walked as one flat float4 index space
-// (128-bit coalesced loads, HW % 4 == 0), one Chan merge per float4 instead of one
-// division per element, a 5-step warp-shuffle tree and a shared-memory stage per warp.
+// (128-bit coalesced loads, HW % 4 == 0) with two loads in flight per thread, one Chan
+// merge per float4 instead of one division per element, a 5-step warp-shuffle tree and
+// a shared-memory stage per warp.
 // Grid-stride over channels, so any common grid works.
 //@ grid=256
 kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) dims (1024, 1, 1) {
@@ -17,12 +18,14 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
   int lane = tid % 32;
   int warp = tid / 32;
   int nwarps = nthr / 32;
-  float v0; float v1; float v2; float v3;
+  float v0; float v1; float v2; float v3; float v4; float v5; float v6; float v7;
   float avg; float m2; int n; float o_avg; float o_m2; int o_n; int tot; float fac; float delta;
   for (int c = blockIdx.x; c < bn_C; c = c + gridDim.x) {
     avg = 0.0;
     m2 = 0.0;
     n = 0;
+    // two float4 cursors per iteration (j and j + nthr of the flat N * HW/4 space):
+    // both loads are in flight before the Welford/Chan updates consume them.
     int b = 0;
     int i = tid;
     while (i >= hw4) {
@@ -30,7 +33,14 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
       b = b + 1;
     }
     while (b < bn_N) {
+      int i2 = i + nthr;
+      int b2 = b;
+      while (i2 >= hw4) {
+        i2 = i2 - hw4;
+        b2 = b2 + 1;
+      }
       vload(bn_x, (b * bn_C + c) * hw4 + i, v0, v1, v2, v3);
+      vload(bn_x, (min(b2, bn_N - 1) * bn_C + c) * hw4 + i2, v4, v5, v6, v7);
       float m4 = ((v0 + v1) + (v2 + v3)) * 0.25;
       float d0 = v0 - m4;
       float d1 = v1 - m4;
@@ -43,7 +53,22 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
       avg = avg + delta * 4.0 * fac;
       m2 = m2 + q + delta * delta * n * 4.0 * fac;
       n = tot;
-      i = i + nthr;
+      if (b2 < bn_N) {
+        m4 = ((v4 + v5) + (v6 + v7)) * 0.25;
+        d0 = v4 - m4;
+        d1 = v5 - m4;
+        d2 = v6 - m4;
+        d3 = v7 - m4;
+        q = (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+        tot = n + 4;
+        delta = m4 - avg;
+        fac = 1.0 / tot;
+        avg = avg + delta * 4.0 * fac;
+        m2 = m2 + q + delta * delta * n * 4.0 * fac;
+        n = tot;
+      }
+      i = i2 + nthr;
+      b = b2;
       while (i >= hw4) {
         i = i - hw4;
         b = b + 1;

@@ -2,8 +2,9 @@
 // 64 bins over [-4, 4]: bin = int((v - lo) * nbins / (hi - lo)), v == hi -> last bin,
 // values outside [lo, hi] are ignored. Because nbins / (hi - lo) = 8 is a power of two,
 // int((v + 4) * 8) is bit-identical to the division form (both scalings are exact).
-// B200 mechanics: 128-bit coalesced loads (n % 4 == 0), warp-private shared-memory bins
-// (32 x 64 counters: intra-warp contention only), one global atomic per bin per block.
+// B200 mechanics: four 128-bit coalesced loads in flight per thread per iteration
+// (n % 4 == 0; tail loads clamped in bounds and masked), warp-private shared-memory bins
+// (32 x 64 counters: contention only inside a warp), one global atomic per bin per block.
 //@ grid=256
 kernel hist(float hi_x[], int hi_out[], int hi_n) dims (1024, 1, 1) {
   shared int hi_bins[2048];
@@ -11,9 +12,18 @@ kernel hist(float hi_x[], int hi_out[], int hi_n) dims (1024, 1, 1) {
   int nthr = blockDim.x * blockDim.y * blockDim.z;
   int wb = (tid / 32) * 64;
   int n4 = hi_n / 4;
-  float v0; float v1; float v2; float v3;
-  for (int i = blockIdx.x * nthr + tid; i < n4; i = i + gridDim.x * nthr) {
+  int last = n4 - 1;
+  int stride = gridDim.x * nthr;
+  float v0; float v1; float v2; float v3; float v4; float v5; float v6; float v7;
+  float v8; float v9; float v10; float v11; float v12; float v13; float v14; float v15;
+  for (int i = blockIdx.x * nthr + tid; i < n4; i = i + 4 * stride) {
+    int j1 = i + stride;
+    int j2 = j1 + stride;
+    int j3 = j2 + stride;
     vload(hi_x, i, v0, v1, v2, v3);
+    vload(hi_x, min(j1, last), v4, v5, v6, v7);
+    vload(hi_x, min(j2, last), v8, v9, v10, v11);
+    vload(hi_x, min(j3, last), v12, v13, v14, v15);
     if (v0 >= -4.0 && v0 <= 4.0) {
       atomic_add(hi_bins[wb + min(int((v0 + 4.0) * 8.0), 63)], 1);
     }
@@ -25,6 +35,48 @@ kernel hist(float hi_x[], int hi_out[], int hi_n) dims (1024, 1, 1) {
     }
     if (v3 >= -4.0 && v3 <= 4.0) {
       atomic_add(hi_bins[wb + min(int((v3 + 4.0) * 8.0), 63)], 1);
+    }
+    if (j1 < n4) {
+      if (v4 >= -4.0 && v4 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v4 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v5 >= -4.0 && v5 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v5 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v6 >= -4.0 && v6 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v6 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v7 >= -4.0 && v7 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v7 + 4.0) * 8.0), 63)], 1);
+      }
+    }
+    if (j2 < n4) {
+      if (v8 >= -4.0 && v8 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v8 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v9 >= -4.0 && v9 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v9 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v10 >= -4.0 && v10 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v10 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v11 >= -4.0 && v11 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v11 + 4.0) * 8.0), 63)], 1);
+      }
+    }
+    if (j3 < n4) {
+      if (v12 >= -4.0 && v12 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v12 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v13 >= -4.0 && v13 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v13 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v14 >= -4.0 && v14 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v14 + 4.0) * 8.0), 63)], 1);
+      }
+      if (v15 >= -4.0 && v15 <= 4.0) {
+        atomic_add(hi_bins[wb + min(int((v15 + 4.0) * 8.0), 63)], 1);
+      }
     }
   }
   syncthreads();

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--form", default="b200")
     ap.add_argument("--splits", default="128,256,384,512,640,768,896")
     ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--regcap", default="off")
     ap.add_argument("--reps", type=int, default=10)
     args = ap.parse_args()
     ma, mb = MEMBERS[args.a], MEMBERS[args.b]
@@ -36,7 +37,7 @@ def main():
     out["b_us"] = hf.time("single", kb, None, img, args.grid, reps=args.reps)["median_us"]
     out["fused"] = {}
     for d1 in map(int, args.splits.split(",")):
-        m = hf.Module.fused(sa, sb, d1, 1024 - d1, grid=args.grid)
+        m = hf.Module.fused(sa, sb, d1, 1024 - d1, regcap=args.regcap, grid=args.grid)
         t = hf.time("single", m, None, img, args.grid, reps=args.reps)["median_us"]
         out["fused"][d1] = {"us": t, "regs": m.info.regs, "bps": m.info.blocks_per_sm}
     best = min(v["us"] for v in out["fused"].values())
