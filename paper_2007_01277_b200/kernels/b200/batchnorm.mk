@@ -1,11 +1,13 @@
 // BatchNorm collect-statistics, B200 form (MK+).
 // Semantics of PyTorch's batch_norm_collect_statistics (PAPER.md:274-325, the corpus
 // analogue /root/reference/proj/corpus/batchnorm.mk): per channel c of x[N, C, HW] the
-// mean and the biased variance, via Welford updates merged with Chan's formula.
+// mean and the biased variance. Each thread accumulates shifted sums over its samples
+// (numerically stable: the shift is one of its own samples) and the per-thread
+// (count, mean, M2) triples are combined with Chan's parallel formula.
 // B200 mechanics: each channel's N planes are walked as one flat float4 index space
-// (128-bit coalesced loads, HW % 4 == 0) with two loads in flight per thread, one Chan
-// merge per float4 instead of one division per element, a 5-step warp-shuffle tree and
-// a shared-memory stage per warp.
+// (128-bit coalesced loads, HW % 4 == 0) with two loads in flight per thread, ~4 FP ops
+// per element (no per-element division as in the naive Welford form), a 5-step
+// warp-shuffle Chan tree and a shared-memory stage per warp.
 // Grid-stride over channels, so any common grid works.
 //@ grid=256
 kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) dims (1024, 1, 1) {
@@ -21,16 +23,21 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
   float v0; float v1; float v2; float v3; float v4; float v5; float v6; float v7;
   float avg; float m2; int n; float o_avg; float o_m2; int o_n; int tot; float fac; float delta;
   for (int c = blockIdx.x; c < bn_C; c = c + gridDim.x) {
-    avg = 0.0;
-    m2 = 0.0;
+    // Per-thread shifted sums (shift = the thread's first sample): s1 = sum(x - K),
+    // s2 = sum((x - K)^2), pairwise within each float4. Two float4 cursors per iteration
+    // (j and j + nthr of the flat N * HW/4 space) keep two 128-bit loads in flight.
     n = 0;
-    // two float4 cursors per iteration (j and j + nthr of the flat N * HW/4 space):
-    // both loads are in flight before the Welford/Chan updates consume them.
+    float K = 0.0;
+    float s1 = 0.0;
+    float s2 = 0.0;
     int b = 0;
     int i = tid;
     while (i >= hw4) {
       i = i - hw4;
       b = b + 1;
+    }
+    if (b < bn_N) {
+      K = bn_x[((b * bn_C + c) * hw4 + i) * 4];
     }
     while (b < bn_N) {
       int i2 = i + nthr;
@@ -41,31 +48,21 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
       }
       vload(bn_x, (b * bn_C + c) * hw4 + i, v0, v1, v2, v3);
       vload(bn_x, (min(b2, bn_N - 1) * bn_C + c) * hw4 + i2, v4, v5, v6, v7);
-      float m4 = ((v0 + v1) + (v2 + v3)) * 0.25;
-      float d0 = v0 - m4;
-      float d1 = v1 - m4;
-      float d2 = v2 - m4;
-      float d3 = v3 - m4;
-      float q = (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
-      tot = n + 4;
-      delta = m4 - avg;
-      fac = 1.0 / tot;
-      avg = avg + delta * 4.0 * fac;
-      m2 = m2 + q + delta * delta * n * 4.0 * fac;
-      n = tot;
+      float e0 = v0 - K;
+      float e1 = v1 - K;
+      float e2 = v2 - K;
+      float e3 = v3 - K;
+      s1 = s1 + ((e0 + e1) + (e2 + e3));
+      s2 = s2 + ((e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3));
+      n = n + 4;
       if (b2 < bn_N) {
-        m4 = ((v4 + v5) + (v6 + v7)) * 0.25;
-        d0 = v4 - m4;
-        d1 = v5 - m4;
-        d2 = v6 - m4;
-        d3 = v7 - m4;
-        q = (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
-        tot = n + 4;
-        delta = m4 - avg;
-        fac = 1.0 / tot;
-        avg = avg + delta * 4.0 * fac;
-        m2 = m2 + q + delta * delta * n * 4.0 * fac;
-        n = tot;
+        e0 = v4 - K;
+        e1 = v5 - K;
+        e2 = v6 - K;
+        e3 = v7 - K;
+        s1 = s1 + ((e0 + e1) + (e2 + e3));
+        s2 = s2 + ((e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3));
+        n = n + 4;
       }
       i = i2 + nthr;
       b = b2;
@@ -74,6 +71,9 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
         b = b + 1;
       }
     }
+    fac = 1.0 / fmaxf(1.0, n);
+    avg = K + s1 * fac;
+    m2 = fmaxf(0.0, s2 - s1 * s1 * fac);
     o_n = warp_shfl_xor(n, 16);
     o_avg = warp_shfl_xor(avg, 16);
     o_m2 = warp_shfl_xor(m2, 16);

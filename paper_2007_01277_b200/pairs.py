@@ -52,6 +52,40 @@ def _hist(n: int, lo: float = -4.0, hi: float = 4.0) -> Callable[[int], Workload
     return make
 
 
+def _maxpool(NC: int, H: int, W: int) -> Callable[[int], Workload]:
+    def make(seed: int = 0) -> Workload:
+        OH, OW = H // 2, W // 2
+        n, m = NC * H * W, NC * OH * OW
+        img = (f"array mp_x float32 {n} seed {3 + seed} uniform -1 1\n"
+               f"array mp_y float32 {m} zero\narray mp_idx int32 {m} zero\n"
+               f"scalar mp_NC int32 {NC}\nscalar mp_H int32 {H}\nscalar mp_W int32 {W}\n"
+               f"scalar mp_OH int32 {OH}\nscalar mp_OW int32 {OW}\n")
+        return Workload(img, 4 * n + 8 * m, f"maxpool 3x3/s2/p1 x[{NC},{H},{W}] fp32 + int32 idx")
+    return make
+
+
+def _upsample(NC: int, IH: int, IW: int) -> Callable[[int], Workload]:
+    def make(seed: int = 0) -> Workload:
+        OH, OW = 2 * IH, 2 * IW
+        n, m = NC * IH * IW, NC * OH * OW
+        img = (f"array us_x float32 {n} seed {4 + seed} uniform -1 1\n"
+               f"array us_y float32 {m} zero\n"
+               f"scalar us_NC int32 {NC}\nscalar us_IH int32 {IH}\nscalar us_IW int32 {IW}\n"
+               f"scalar us_OH int32 {OH}\nscalar us_OW int32 {OW}\n")
+        return Workload(img, 4 * n + 4 * m, f"upsample bilinear 2x x[{NC},{IH},{IW}] fp32")
+    return make
+
+
+def _im2col(NC: int, H: int, W: int) -> Callable[[int], Workload]:
+    def make(seed: int = 0) -> Workload:
+        n, m = NC * H * W, NC * 9 * H * W
+        img = (f"array ic_x float32 {n} seed {5 + seed} uniform -1 1\n"
+               f"array ic_col float32 {m} zero\n"
+               f"scalar ic_NC int32 {NC}\nscalar ic_H int32 {H}\nscalar ic_W int32 {W}\n")
+        return Workload(img, 4 * n + 4 * m, f"im2col 3x3/p1 x[{NC},{H},{W}] fp32")
+    return make
+
+
 MEMBERS: Dict[str, Member] = {
     "bn": Member("bn", "batchnorm", {
         "full": _bn(64, 256, 56 * 56),
@@ -63,7 +97,24 @@ MEMBERS: Dict[str, Member] = {
         "parity": _hist(2 * 8 * 56 * 56, -4.5, 4.5),
         "tiny": _hist(64, -5.0, 5.0),
     }),
+
+    "maxpool": Member("maxpool", "maxpool", {
+        "full": _maxpool(64 * 64, 112, 112),
+        "parity": _maxpool(3, 16, 16),
+        "tiny": _maxpool(1, 8, 8),
+    }),
+    "upsample": Member("upsample", "upsample", {
+        "full": _upsample(64 * 256, 28, 28),
+        "parity": _upsample(3, 8, 8),
+        "tiny": _upsample(1, 4, 4),
+    }),
+    "im2col": Member("im2col", "im2col", {
+        "full": _im2col(32 * 64, 56, 56),
+        "parity": _im2col(3, 8, 8),
+        "tiny": _im2col(1, 4, 4),
+    }),
 }
 
-# The ten DL pairs of the paper, over the members built so far.
-PAIRS = [("bn", "hist")]
+ORDER = ["bn", "hist", "im2col", "maxpool", "upsample"]
+# The ten DL pairs of the paper.
+PAIRS = [(a, b) for i, a in enumerate(ORDER) for b in ORDER[i + 1:]]

@@ -1,0 +1,117 @@
+"""Device parity of the DL members and the ten fused DL pairs.
+
+Small sizes: bit-exact against the reference interpreter (tests/golden/members.json,
+made by tests/golden/make_members.py from oracle/_ref). Full sizes (the bench workload):
+against the C restatement oracle/hf_oracle.c — exact for Hist, MaxPool (values and
+indices), Upsample and Im2Col; BatchNorm mean/var within 1e-5 * max(1, |x|) of the fp64
+two-pass statistics (the tolerance form of test_fuser.cpp:459).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import oracle
+from paper_2007_01277_b200 import pairs
+
+G = golden("members.json")
+GRID = G["grid"]
+BN_TOL = 1e-5
+
+
+def from_bits(v):
+    return np.array(v, np.uint32)
+
+
+def outputs(img, names):
+    return {n: img.array(n).view(np.uint32) for n in names}
+
+
+def image(hf, *keys, size="parity"):
+    img = hf.Image(pairs.MEMBERS[keys[0]].sizes[size](0).image)
+    for k in keys[1:]:
+        img.merge(hf.Image(pairs.MEMBERS[k].sizes[size](0).image))
+    return img
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form", ["ref", "b200"])
+@pytest.mark.parametrize("size", ["tiny", "parity"])
+@pytest.mark.parametrize("key", list(pairs.MEMBERS))
+def test_member_matches_interpreter(gpu, key, size, form):
+    hf = gpu
+    mod = hf.Module.kernel(pairs.source(form, pairs.MEMBERS[key].stem), grid=GRID)
+    img = image(hf, key, size=size).upload()
+    mod.run(img, GRID)
+    img.download()
+    assert img.digest_hex() == G["members"][key][size][form]["digest"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d1", G["splits"])
+@pytest.mark.parametrize("pair", [f"{a}+{b}" for a, b in pairs.PAIRS])
+def test_fused_pair_matches_sequential_interpreter(gpu, pair, d1):
+    hf = gpu
+    a, b = pair.split("+")
+    sa = pairs.source("b200", pairs.MEMBERS[a].stem)
+    sb = pairs.source("b200", pairs.MEMBERS[b].stem)
+    mod = hf.Module.fused(sa, sb, d1, 1024 - d1, grid=GRID)
+    img = image(hf, a, b).upload()
+    mod.run(img, GRID)
+    img.download()
+    assert img.digest_hex() == G["pairs"][pair][str(d1)]["digest"]
+
+
+def test_b200_forms_agree_with_naive_forms():
+    """B200 member outputs vs the naive (reference-form) outputs, both from the reference
+    interpreter: exact except BatchNorm (different summation order, tolerance)."""
+    for key, sizes in G["members"].items():
+        for size, row in sizes.items():
+            for name, ref_bits in row["ref"]["outputs"].items():
+                got = from_bits(row["b200"]["outputs"][name])
+                want = from_bits(ref_bits)
+                if key == "bn":
+                    g, w = got.view(np.float32), want.view(np.float32)
+                    assert np.all(np.abs(g - w) <= BN_TOL * np.maximum(1.0, np.abs(w))), (key, size)
+                else:
+                    assert np.array_equal(got, want), (key, size, name)
+
+
+def check_full(key, img, oracle_inputs=None):
+    """Compare one member's full-size device outputs with the C restatement."""
+    w = pairs.MEMBERS[key].sizes["full"](0)
+    arrays, scalars = oracle.parse_image(w.image)
+    if key == "bn":
+        mean, var = oracle.bn_stats(arrays["bn_x"], int(scalars["bn_N"]), int(scalars["bn_C"]), int(scalars["bn_HW"]))
+        got = img.array("bn_stats").reshape(-1, 2).astype(np.float64)
+        for g, want in ((got[:, 0], mean), (got[:, 1], var)):
+            assert np.all(np.abs(g - want) <= BN_TOL * np.maximum(1.0, np.abs(want)))
+    elif key == "hist":
+        want = oracle.hist(arrays["hi_x"])
+        assert np.array_equal(img.array("hi_out"), want)
+        assert int(want.sum()) == int(scalars["hi_n"])  # uniform on [-4, 4]: every sample counted
+    elif key == "maxpool":
+        y, idx = oracle.maxpool(arrays["mp_x"], int(scalars["mp_NC"]), int(scalars["mp_H"]), int(scalars["mp_W"]))
+        assert np.array_equal(img.array("mp_y").view(np.uint32), y.view(np.uint32))
+        assert np.array_equal(img.array("mp_idx"), idx)
+    elif key == "upsample":
+        y = oracle.upsample(arrays["us_x"], int(scalars["us_NC"]), int(scalars["us_IH"]), int(scalars["us_IW"]))
+        assert np.array_equal(img.array("us_y").view(np.uint32), y.view(np.uint32))
+    elif key == "im2col":
+        col = oracle.im2col(arrays["ic_x"], int(scalars["ic_NC"]), int(scalars["ic_H"]), int(scalars["ic_W"]))
+        assert np.array_equal(img.array("ic_col").view(np.uint32), col.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pair", [f"{a}+{b}" for a, b in pairs.PAIRS])
+def test_full_size_fused_pair_matches_c_oracle(gpu, pair):
+    """The bench workload itself: fused (d1 = 512) at the C1/C2 sizes, grid 296."""
+    hf = gpu
+    a, b = pair.split("+")
+    sa = pairs.source("b200", pairs.MEMBERS[a].stem)
+    sb = pairs.source("b200", pairs.MEMBERS[b].stem)
+    mod = hf.Module.fused(sa, sb, 512, 512, grid=296)
+    img = image(hf, a, b, size="full").upload()
+    mod.run(img, 296)
+    img.download()
+    check_full(a, img)
+    check_full(b, img)
