@@ -91,12 +91,28 @@ def make_corpus():
                 fz = run("fused", f"{CORPUS}/{a}.mk", f"{CORPUS}/{b}.mk", "--d1", d1, "--d2", d2, *mem, "--seed", seed)
                 rows[str(seed)] = {"sequential": s["out"].split()[-1], "fused": fz["out"].split()[-1]}
             dig["pairs"][f"{a}+{b}"] = {"d1": d1, "d2": d2, "seeds": rows}
+    dig["images"] = {}
+    for a in STEMS:
+        rows = {}
+        for seed in (None, 1, 5):
+            extra = [] if seed is None else ["--seed", seed]
+            r = run("run", f"{CORPUS}/empty.mk", "--mem", f"{CORPUS}/images/{a}.img", *extra)
+            rows[str(seed)] = r["out"].split()[-1]
+        dig["images"][a] = rows
     for a in STEMS:
         rows = {}
         for seed in range(1, 6):
             r = run("run", f"{CORPUS}/{a}.mk", "--mem", f"{CORPUS}/images/{a}.img", "--seed", seed)
             rows[str(seed)] = r["out"].split()[-1]
         dig["kernels"][a] = rows
+    # reference numbers for the machine model (machine.cpp:236-283)
+    dig["register_bound"] = {}
+    for case in [(32, 896, 24, 128, 4096), (16, 512, 16, 512, 256), (16, 512, 16, 512, 60000),
+                 (40, 768, 20, 256, 0), (64, 128, 8, 896, 1024)]:
+        dig["register_bound"][",".join(map(str, case))] = int(run("regbound", *case)["out"])
+    dig["occupancy"] = {}
+    for case in [(64, 24576, 512), (32, 24576, 512), (21, 640, 1024), (255, 0, 256), (16, 98304, 32)]:
+        dig["occupancy"][",".join(map(str, case))] = run("occupancy", *case).get("out", "").strip()
     with open(os.path.join(HERE, "corpus_digests.json"), "w") as f:
         json.dump(dig, f, indent=1, sort_keys=True)
     print("corpus fixtures written")

@@ -1,0 +1,50 @@
+"""The C ABI boundary (include/hfuse.h): the in-tree library loads on a GPU-less host and
+exports every declared entry point; no compute calls here."""
+import ctypes
+import os
+import re
+import subprocess
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "hfuse.h")
+
+
+def declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(hf_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(hf):
+    lib = ctypes.CDLL(hf.LIB_PATH)
+    names = declared()
+    assert len(names) >= 35
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", hf.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (hf_\w+)", out))
+    assert set(names) <= exported
+
+
+def test_python_mirror_binds_the_whole_header(hf):
+    assert sorted(hf.EXPORTS) == declared()
+
+
+def test_version_and_device_count_without_gpu(hf):
+    assert "sm_100a" in hf.lib().hf_version().decode()
+    assert hf.device_count() >= 0
+
+
+def test_errors_cross_the_abi_as_codes(hf):
+    try:
+        hf.fuse("kernel a() dims (32, 1, 1) { x = 1; }", "kernel b() dims (32, 1, 1) { }", 32, 32)
+    except hf.HFuseError as e:
+        assert e.name == "UnknownIdentifier" and (e.line, e.col) == (1, 30)
+    else:
+        raise AssertionError("expected an error")
+
+
+def test_cli_binary_present():
+    exe = os.path.join(ROOT, "paper_2007_01277_b200", "bin", "hfuse")
+    r = subprocess.run([exe, "nope"], capture_output=True, text=True)
+    assert r.returncode == 1 and r.stderr.startswith("error[InvalidArgument]")

@@ -1,0 +1,120 @@
+"""Frontend, normalization and the MK+ dialect."""
+import os
+
+import pytest
+
+from conftest import golden
+
+from oracle import oracle
+
+
+@pytest.mark.parametrize("src,code", [
+    ("kernel k() dims (32, 1, 1) { int x = ; }", "Syntax"),
+    ("kernel k() dims (32, 1, 1) { x = 1; }", "UnknownIdentifier"),
+    ("kernel k(int a[]) dims (32, 1, 1) { int x = 1.5; }", "TypeMismatch"),
+    ("kernel k() dims (32, 1, 1) { goto nowhere; }", "UnresolvedLabel"),
+    ("kernel k() dims (32, 1, 1) { bar_sync(16, 32); }", "BadBarrierId"),
+    ("kernel k() dims (32, 1, 1) { bar_sync(1, 48); }", "MisalignedCount"),
+    ("kernel k(int a[]) dims (32, 1, 1) { a[0] = warp_shfl_xor(a[0], 32); }", "TypeMismatch"),
+    ("int f(int x) { return g(x); }\nint g(int x) { return f(x); }\nkernel k() dims (32, 1, 1) { }", "Recursion"),
+    ("kernel k() dims (4096, 1, 1) { }", "ThreadBudgetExceeded"),
+    ("kernel k() dims (32, 1, 1) { }\nkernel k() dims (32, 1, 1) { }", "DuplicateName"),
+    ("kernel k() dims (32, 1, 1) { int x = 99999999999; }", "Syntax"),
+])
+def test_rejections_map_to_reference_codes(hf, src, code):
+    with pytest.raises(hf.HFuseError) as e:
+        hf.check(src)
+    assert e.value.name == code
+
+
+def test_strict_mode_rejects_dialect_extensions(hf):
+    src = "kernel k(int a[]) dims (32, 1, 1) { a[0] = shr_u(a[0], 3); }"
+    assert hf.check(src).startswith("ok")
+    with pytest.raises(hf.HFuseError) as e:
+        hf.check(src, strict=True)
+    assert e.value.name == "UnresolvedCall"
+    with pytest.raises(hf.HFuseError):
+        hf.check("kernel k(int a[]) dims (32, 1, 1) { a[0] = 0x10; }", strict=True)
+
+
+def test_lint_flags_goto_over_declaration(hf):
+    src = "kernel k() dims (32, 1, 1) { goto L; int x = 1; L: }"
+    assert "jumps over a declaration" in hf.check(src)
+
+
+def test_normalization_names_match_reference(hf, corpus):
+    text = hf.normalize(corpus["kernels"]["histogram"], "k2_")
+    for name in ("k2___ret__inl0", "k2_value__inl0", "k2_nbins__inl0", "k2_b__inl0", "k2_i_2", "k2_i_3"):
+        assert name in text
+
+
+MKPLUS = """
+kernel ext(int xi[], int xo[], float fi[], float fo[]) dims (32, 1, 1) {
+  int t = threadIdx.x;
+  int a = xi[t];
+  int b = xi[t + 32];
+  xo[t * 8] = shr_u(a, b);
+  xo[t * 8 + 1] = shr_u(a, 7);
+  xo[t * 8 + 2] = rotr(a, b);
+  xo[t * 8 + 3] = rotl(a, 13);
+  xo[t * 8 + 4] = ltu(a, b);
+  xo[t * 8 + 5] = rotr(a, 0) ^ 0xdeadbeef;
+  float v0; float v1; float v2; float v3;
+  vload(fi, t, v0, v1, v2, v3);
+  vstore(fo, t, v3, v2 + v1, v1, v0 * 2.0);
+  unroll 4 for (int i = 0; i < 4; i = i + 1) {
+    xo[t * 8 + 6] = xo[t * 8 + 6] + i;
+  }
+}
+"""
+IMG = ("array xi int32 64 seed 9 range -2147483648 2147483647\narray xo int32 256 zero\n"
+       "array fi float32 128 seed 3 uniform -2 2\narray fo float32 128 zero\n")
+
+
+def ref_semantics(xi, fi):
+    import numpy as np
+    u = xi.astype(np.int64) & 0xFFFFFFFF
+    out = np.zeros(256, np.int64)
+    for t in range(32):
+        a, b = int(u[t]), int(u[t + 32])
+        s = b & 31
+        out[t * 8] = a >> s
+        out[t * 8 + 1] = a >> 7
+        out[t * 8 + 2] = ((a >> s) | (a << (32 - s))) & 0xFFFFFFFF
+        out[t * 8 + 3] = ((a << 13) | (a >> 19)) & 0xFFFFFFFF
+        out[t * 8 + 4] = int(a < b)
+        out[t * 8 + 5] = a ^ 0xDEADBEEF
+        out[t * 8 + 6] = 6
+    fo = np.zeros(128, np.float32)
+    for t in range(32):
+        v = fi[4 * t:4 * t + 4]
+        fo[4 * t:4 * t + 4] = [v[3], np.float32(v[2] + v[1]), v[1], np.float32(v[0] * 2)]
+    return out.astype(np.uint32).view(np.int32), fo
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_mkplus_lowering_runs_on_reference_interpreter(hf, tmp_path):
+    """MK+ -> Mini-Kernel (hf_lower) executes on the reference's run_functional with the
+    dialect's documented semantics (logical shifts, rotates, unsigned compare, vectors)."""
+    import numpy as np
+    low = hf.lower(MKPLUS)
+    assert hf.check(low, strict=True).startswith("ok")
+    k = tmp_path / "k.mk"
+    k.write_text(low)
+    im = tmp_path / "k.img"
+    im.write_text(IMG)
+    _, _, dump = oracle.ref_run("run", k, "--mem", im)
+    arrays, _ = oracle.parse_image(dump)
+    inputs, _ = oracle.parse_image(IMG)
+    xo, fo = ref_semantics(inputs["xi"], inputs["fi"])
+    assert np.array_equal(arrays["xo"], xo)
+    assert np.array_equal(arrays["fo"].view(np.uint32), fo.view(np.uint32))
+
+
+def test_member_kernels_parse_and_lower(hf):
+    from paper_2007_01277_b200 import pairs
+    for m in pairs.MEMBERS.values():
+        for form in ("ref", "b200"):
+            src = pairs.source(form, m.stem)
+            assert hf.check(src).startswith("ok: 1 kernel(s)")
+            assert hf.check(hf.lower(src), strict=True).startswith("ok: 1 kernel(s)")
