@@ -99,6 +99,7 @@ typedef struct hf_search_opts {
   int reps;
   int flush_l2;
   int measured_registers;   /* r0 from ptxas register counts instead of the estimate */
+  int specialize;           /* fold the image's scalar values into every candidate */
   int n_extra_caps;
   const int* extra_caps;    /* additional register caps per partition (C4 sweep) */
   int out_style;            /* style of *best_src */
@@ -159,20 +160,23 @@ int hf_device_count(void);
 int hf_get_device_props(hf_device_props* out, hf_error* err);
 
 /* Fuse, emit for sm_100a and NVRTC-compile (regcap: HF_REGCAP_OFF, HF_REGCAP_AUTO = the
- * register bound r0 of machine.cpp:269-283, or an explicit cap). grid 0 = annotation. */
+ * register bound r0 of machine.cpp:269-283, or an explicit cap). grid 0 = annotation.
+ * specialize (may be NULL): fold that image's scalar values into the code as constants
+ * (JIT specialization; hf_run/hf_launch then require the same values). */
 int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regcap, int grid,
-                   int min_blocks, hf_module** out, hf_error* err);
+                   int min_blocks, const hf_image* specialize, hf_module** out, hf_error* err);
 /* One unfused kernel at its declared dims (regcap: HF_REGCAP_OFF or a cap). */
-int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks, hf_module** out,
-                    hf_error* err);
+int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks,
+                    const hf_image* specialize, hf_module** out, hf_error* err);
 int hf_module_get_info(const hf_module* m, hf_module_info* out);
 const char* hf_module_source(const hf_module* m);  /* borrowed */
 const char* hf_module_entry(const hf_module* m);   /* borrowed */
 int hf_module_param(const hf_module* m, int i, const char** name, int* is_array, int* is_float,
-                    int* is_written);
+                    int* is_written, int* is_specialized);
 int hf_module_barrier(const hf_module* m, int i, hf_barrier* out);
 int hf_module_cubin(const hf_module* m, const void** data, size_t* size);
-/* Raw launch: args[i] points at the i-th parameter value (device pointer or scalar). */
+/* Raw launch: args[i] points at the i-th parameter value (device pointer or scalar);
+ * specialized scalars are checked against the folded value. */
 int hf_launch(const hf_module* m, int grid, void** args, void* stream, hf_error* err);
 void hf_module_free(hf_module* m);
 
@@ -205,7 +209,8 @@ int hf_time(int mode, const hf_module* a, const hf_module* b, hf_image* img, int
 
 /* ProfilerBackend::evaluate (search.hpp:19-23) for one candidate on the device. */
 int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, hf_image* img,
-               int grid, int warmup, int reps, int flush_l2, hf_eval* out, hf_error* err);
+               int grid, int warmup, int reps, int flush_l2, int specialize, hf_eval* out,
+               hf_error* err);
 
 /* search_config / fixed_partition_fuse + trace_csv (search.hpp:66-77). img may be NULL for
  * the command backend. */

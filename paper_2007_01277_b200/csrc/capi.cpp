@@ -70,13 +70,22 @@ hf::Style style_of(int s) {
   return s == HF_STYLE_STRUCTURED ? hf::Style::Structured : s == HF_STYLE_GOTO ? hf::Style::Goto : hf::Style::Sm100;
 }
 
+std::map<std::string, hf::ScalarVal> scalars_of(const hf_image* img) {
+  std::map<std::string, hf::ScalarVal> m;
+  if (!img) return m;
+  for (const auto& [n, s] : img->img.scalars) m[n] = hf::ScalarVal{s.ty, s.i, s.f};
+  return m;
+}
+
 // sm_100a fused module; regcap AUTO means the register bound r0 with the B200 machine model.
-hf::rt::Module build_fused(const char* s1, const char* s2, int d1, int d2, int regcap, int grid, int min_blocks) {
+hf::rt::Module build_fused(const char* s1, const char* s2, int d1, int d2, int regcap, int grid, int min_blocks,
+                           const hf_image* spec) {
   hf::SM sm = hf::rt::device_available() ? hf::rt::sm_from_device() : hf::SM::b200();
   hf::FuseResult r = hf::fuse_sources(s1, s2, d1, d2, regcap_spec(regcap), sm);
   if (grid > 0) r.fused.grid = grid;
   hf::Sm100Options o;
   o.min_blocks = min_blocks;
+  o.specialize = scalars_of(spec);
   return hf::rt::compile(hf::emit_sm100(r.fused, o), r.fused.cfg.reg_cap);
 }
 
@@ -182,20 +191,22 @@ int hf_get_device_props(hf_device_props* out, hf_error* err) {
 }
 
 int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regcap, int grid, int min_blocks,
-                   hf_module** out, hf_error* err) {
+                   const hf_image* specialize, hf_module** out, hf_error* err) {
   return guarded(err, [&] {
     auto h = std::make_unique<hf_module>();
-    h->m = build_fused(src1, src2, d1, d2, regcap, grid, min_blocks);
+    h->m = build_fused(src1, src2, d1, d2, regcap, grid, min_blocks, specialize);
     *out = h.release();
   });
 }
 
-int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks, hf_module** out, hf_error* err) {
+int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks, const hf_image* specialize,
+                    hf_module** out, hf_error* err) {
   return guarded(err, [&] {
     hf::Loaded l = hf::load_source(src);
     if (grid > 0) l.kernel.grid = grid;
     hf::Sm100Options o;
     o.min_blocks = min_blocks;
+    o.specialize = scalars_of(specialize);
     std::optional<int> cap;
     if (regcap > 0) cap = regcap;
     auto h = std::make_unique<hf_module>();
@@ -214,9 +225,11 @@ int hf_module_get_info(const hf_module* m, hf_module_info* out) {
 const char* hf_module_source(const hf_module* m) { return m ? m->m.source.c_str() : nullptr; }
 const char* hf_module_entry(const hf_module* m) { return m ? m->m.entry.c_str() : nullptr; }
 
-int hf_module_param(const hf_module* m, int i, const char** name, int* is_array, int* is_float, int* is_written) {
+int hf_module_param(const hf_module* m, int i, const char** name, int* is_array, int* is_float, int* is_written,
+                    int* is_specialized) {
   if (!m || i < 0 || i >= int(m->m.params.size())) return to_abi(hf::Code::InvalidArgument);
   const auto& p = m->m.params[size_t(i)];
+  if (is_specialized) *is_specialized = p.specialized;
   if (name) *name = p.name.c_str();
   if (is_array) *is_array = p.array;
   if (is_float) *is_float = p.ty == hf::Ty::Float;
@@ -239,7 +252,17 @@ int hf_module_cubin(const hf_module* m, const void** data, size_t* size) {
 }
 
 int hf_launch(const hf_module* m, int grid, void** args, void* stream, hf_error* err) {
-  return guarded(err, [&] { hf::rt::launch_raw(m->m, grid > 0 ? grid : m->m.grid, args, stream); });
+  return guarded(err, [&] {
+    for (size_t i = 0; i < m->m.params.size(); ++i) {
+      const auto& p = m->m.params[i];
+      if (!p.specialized) continue;
+      bool same = p.ty == hf::Ty::Int ? *static_cast<const int32_t*>(args[i]) == p.value.i
+                                      : std::memcmp(args[i], &p.value.f, 4) == 0;
+      if (!same)
+        hf::raise(hf::Code::InvalidArgument, "module is specialized for a different value of scalar '" + p.name + "'");
+    }
+    hf::rt::launch_raw(m->m, grid > 0 ? grid : m->m.grid, args, stream);
+  });
 }
 
 void hf_module_free(hf_module* m) {
@@ -347,9 +370,9 @@ int hf_time(int mode, const hf_module* a, const hf_module* b, hf_image* img, int
 }
 
 int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, hf_image* img, int grid, int warmup,
-               int reps, int flush_l2, hf_eval* out, hf_error* err) {
+               int reps, int flush_l2, int specialize, hf_eval* out, hf_error* err) {
   return guarded(err, [&] {
-    hf::rt::Module m = build_fused(src1, src2, d1, d2, regcap, grid, 0);
+    hf::rt::Module m = build_fused(src1, src2, d1, d2, regcap, grid, 0, specialize ? img : nullptr);
     hf::rt::Timing t =
         hf::rt::time(hf::rt::Mode::Single, m, nullptr, img->img, grid, 0, warmup, reps, flush_l2 != 0, nullptr);
     hf::rt::Props p = hf::rt::props();
@@ -378,8 +401,11 @@ int hf_search(const char* src1, const char* src2, hf_image* img, const hf_search
       be = std::make_unique<hf::ExternalCommandBackend>(o.profiler_cmd ? o.profiler_cmd : "");
     } else {
       if (!img) hf::raise(hf::Code::InvalidArgument, "the device backend needs a memory image");
-      be = std::make_unique<hf::DeviceBackend>(img->img, o.grid, o.warmup > 0 ? o.warmup : 3,
-                                               o.reps > 0 ? o.reps : 10, o.flush_l2 != 0, o.measured_registers != 0);
+      auto dev = std::make_unique<hf::DeviceBackend>(img->img, o.grid, o.warmup > 0 ? o.warmup : 3,
+                                                     o.reps > 0 ? o.reps : 10, o.flush_l2 != 0,
+                                                     o.measured_registers != 0);
+      if (o.specialize) dev->set_specialization(scalars_of(img));
+      be = std::move(dev);
     }
     hf::SearchOptions so;
     so.granularity = o.granularity > 0 ? o.granularity : 128;

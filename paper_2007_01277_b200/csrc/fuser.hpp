@@ -8,6 +8,7 @@
 //  * an `sm100` emitter (emit_sm100.cpp) next to the byte-compatible goto / structured ones.
 #pragma once
 
+#include <map>
 #include <optional>
 #include <string>
 #include <vector>
@@ -99,17 +100,28 @@ std::string emit_goto(const Fused& f);        // byte-compatible with fuser.cpp:
 std::string emit_structured(const Fused& f);  // emit_minikernel(to_kernel())
 
 // ---- sm_100a emission -----------------------------------------------------------
+struct ScalarVal {
+  Ty ty = Ty::Int;
+  int32_t i = 0;
+  float f = 0.0f;
+};
+
 struct Sm100Options {
   std::string entry;       // extern "C" symbol (default: the kernel name)
   int min_blocks = 0;      // __launch_bounds__(threads, min_blocks) when > 0
   bool zero_shared = true; // the interpreter zero-initializes shared memory per block
+  // JIT specialization: scalar parameters (never assigned by the kernel) whose launch
+  // values are folded into the code as constants; the runtime checks them at bind time.
+  std::map<std::string, ScalarVal> specialize;
 };
 
 struct Sm100Param {
   std::string name;
   Ty ty;
   bool array;
-  bool written;  // array parameters only
+  bool written;             // array parameters only
+  bool specialized = false; // scalar folded into the code (value below)
+  ScalarVal value;
 };
 
 struct Sm100Kernel {

@@ -321,6 +321,9 @@ Bound bind(const Module& m, Image& img) {
       if (it == img.scalars.end())
         raise(Code::InvalidArgument, "memory image does not provide scalar '" + p.name + "'");
       if (it->second.ty != p.ty) raise(Code::TypeMismatch, "scalar '" + p.name + "' type mismatch");
+      if (p.specialized && (p.ty == Ty::Int ? it->second.i != p.value.i
+                                            : std::memcmp(&it->second.f, &p.value.f, 4) != 0))
+        raise(Code::InvalidArgument, "module is specialized for a different value of scalar '" + p.name + "'");
       if (p.ty == Ty::Int) b.cells[i] = it->second.i;
       else std::memcpy(&b.cells[i], &it->second.f, 4);
       b.args[i] = &b.cells[i];

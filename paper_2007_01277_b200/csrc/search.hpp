@@ -51,8 +51,10 @@ class DeviceBackend : public ProfilerBackend {
                 bool measured_registers = true);
   EvalOutcome evaluate(const Fused& fused, const FusionConfig& cfg) override;
   Resources resources(const Kernel& k, int threads) override;
+  void set_specialization(std::map<std::string, ScalarVal> s) { spec_ = std::move(s); }
 
  private:
+  std::map<std::string, ScalarVal> spec_;
   Image& img_;
   int grid_, warmup_, reps_;
   bool flush_, measured_;

@@ -90,7 +90,7 @@ class _SearchOpts(C.Structure):
     _fields_ = [("d0", C.c_int), ("granularity", C.c_int), ("backend", C.c_int),
                 ("profiler_cmd", C.c_char_p), ("grid", C.c_int), ("warmup", C.c_int),
                 ("reps", C.c_int), ("flush_l2", C.c_int), ("measured_registers", C.c_int),
-                ("n_extra_caps", C.c_int), ("extra_caps", C.POINTER(C.c_int)),
+                ("specialize", C.c_int), ("n_extra_caps", C.c_int), ("extra_caps", C.POINTER(C.c_int)),
                 ("out_style", C.c_int)]
 
 
@@ -120,12 +120,13 @@ def _load() -> C.CDLL:
         "hf_occupancy": (ip, [ip, C.c_longlong, ip, cp, C.POINTER(_Occ), E]),
         "hf_device_count": (ip, []),
         "hf_get_device_props": (ip, [C.POINTER(_Props), E]),
-        "hf_build_fused": (ip, [cp, cp, ip, ip, ip, ip, ip, C.POINTER(vp), E]),
-        "hf_build_kernel": (ip, [cp, ip, ip, ip, C.POINTER(vp), E]),
+        "hf_build_fused": (ip, [cp, cp, ip, ip, ip, ip, ip, vp, C.POINTER(vp), E]),
+        "hf_build_kernel": (ip, [cp, ip, ip, ip, vp, C.POINTER(vp), E]),
         "hf_module_get_info": (ip, [vp, C.POINTER(_ModInfo)]),
         "hf_module_source": (cp, [vp]),
         "hf_module_entry": (cp, [vp]),
-        "hf_module_param": (ip, [vp, ip, C.POINTER(cp), C.POINTER(ip), C.POINTER(ip), C.POINTER(ip)]),
+        "hf_module_param": (ip, [vp, ip, C.POINTER(cp), C.POINTER(ip), C.POINTER(ip), C.POINTER(ip),
+                                 C.POINTER(ip)]),
         "hf_module_barrier": (ip, [vp, ip, C.POINTER(_Barrier)]),
         "hf_module_cubin": (ip, [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]),
         "hf_launch": (ip, [vp, ip, C.POINTER(vp), vp, E]),
@@ -147,7 +148,7 @@ def _load() -> C.CDLL:
         "hf_image_free": (None, [vp]),
         "hf_run": (ip, [vp, vp, ip, vp, E]),
         "hf_time": (ip, [ip, vp, vp, vp, ip, ip, ip, ip, ip, vp, C.POINTER(_Timing), E]),
-        "hf_profile": (ip, [cp, cp, ip, ip, ip, vp, ip, ip, ip, ip, C.POINTER(_Eval), E]),
+        "hf_profile": (ip, [cp, cp, ip, ip, ip, vp, ip, ip, ip, ip, ip, C.POINTER(_Eval), E]),
         "hf_search": (ip, [cp, cp, vp, C.POINTER(_SearchOpts), C.POINTER(ip), C.POINTER(ip), C.POINTER(ip),
                            C.POINTER(C.c_longlong), C.POINTER(vp), C.POINTER(vp), E]),
     }
@@ -390,17 +391,20 @@ class Module:
 
     @classmethod
     def fused(cls, src1: str, src2: str, d1: int, d2: int, regcap="off", grid: int = 0,
-              min_blocks: int = 0) -> "Module":
+              min_blocks: int = 0, specialize: Optional["Image"] = None) -> "Module":
+        """specialize: fold that image's scalar values into the code (JIT specialization)."""
         h, err = C.c_void_p(), _Err()
         _check(_lib.hf_build_fused(src1.encode(), src2.encode(), d1, d2, _regcap(regcap), grid, min_blocks,
-                                   C.byref(h), C.byref(err)), err)
+                                   specialize._h if specialize else None, C.byref(h), C.byref(err)), err)
         return cls(h)
 
     @classmethod
-    def kernel(cls, src: str, regcap=None, grid: int = 0, min_blocks: int = 0) -> "Module":
+    def kernel(cls, src: str, regcap=None, grid: int = 0, min_blocks: int = 0,
+               specialize: Optional["Image"] = None) -> "Module":
         h, err = C.c_void_p(), _Err()
         cap = -1 if regcap in (None, "off") else int(regcap)
-        _check(_lib.hf_build_kernel(src.encode(), cap, grid, min_blocks, C.byref(h), C.byref(err)), err)
+        _check(_lib.hf_build_kernel(src.encode(), cap, grid, min_blocks, specialize._h if specialize else None,
+                                    C.byref(h), C.byref(err)), err)
         return cls(h)
 
     @property
@@ -421,10 +425,10 @@ class Module:
     def params(self) -> List[dict]:
         out = []
         for i in range(self.info.n_params):
-            n, a, f, w = C.c_char_p(), C.c_int(), C.c_int(), C.c_int()
-            _lib.hf_module_param(self._h, i, C.byref(n), C.byref(a), C.byref(f), C.byref(w))
+            n, a, f, w, sp = C.c_char_p(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+            _lib.hf_module_param(self._h, i, C.byref(n), C.byref(a), C.byref(f), C.byref(w), C.byref(sp))
             out.append({"name": n.value.decode(), "array": bool(a.value), "float": bool(f.value),
-                        "written": bool(w.value)})
+                        "written": bool(w.value), "specialized": bool(sp.value)})
         return out
 
     @property
@@ -480,10 +484,10 @@ def time(mode: str, a: Module, b: Optional[Module], img: Image, grid_a: int = 0,
 
 
 def profile(src1: str, src2: str, d1: int, d2: int, img: Image, regcap="off", grid: int = 0,
-            warmup: int = 3, reps: int = 10, flush_l2: bool = True) -> dict:
+            warmup: int = 3, reps: int = 10, flush_l2: bool = True, specialize: bool = False) -> dict:
     e, err = _Eval(), _Err()
     _check(_lib.hf_profile(src1.encode(), src2.encode(), d1, d2, _regcap(regcap), img._h, grid, warmup, reps,
-                           int(flush_l2), C.byref(e), C.byref(err)), err)
+                           int(flush_l2), int(specialize), C.byref(e), C.byref(err)), err)
     return {"cycles": e.cycles, "occupancy": e.occupancy, "utilization": e.utilization, "us": e.us,
             "regs": e.regs}
 
@@ -491,10 +495,11 @@ def profile(src1: str, src2: str, d1: int, d2: int, img: Image, regcap="off", gr
 def search(src1: str, src2: str, img: Optional[Image] = None, d0: int = 1024, granularity: int = 128,
            profiler_cmd: Optional[str] = None, grid: int = 0, warmup: int = 3, reps: int = 10,
            flush_l2: bool = True, measured_registers: bool = True, extra_caps: Sequence[int] = (),
-           out_style: str = "structured") -> dict:
+           out_style: str = "structured", specialize: bool = False) -> dict:
     caps = (C.c_int * max(1, len(extra_caps)))(*extra_caps)
     o = _SearchOpts(d0, granularity, 1 if profiler_cmd else 0, _b(profiler_cmd), grid, warmup, reps,
-                    int(flush_l2), int(measured_registers), len(extra_caps), caps, STYLES[out_style])
+                    int(flush_l2), int(measured_registers), int(specialize), len(extra_caps), caps,
+                    STYLES[out_style])
     d1, d2, cap, best = C.c_int(), C.c_int(), C.c_int(), C.c_longlong()
     trace, src, err = C.c_void_p(), C.c_void_p(), _Err()
     _check(_lib.hf_search(src1.encode(), src2.encode(), img._h if img else None, C.byref(o), C.byref(d1),
