@@ -22,11 +22,11 @@ for k in need[1:]:
     img.merge(hf.Image(P.MEMBERS[k].sizes["full"](0).image))
 img.upload()
 for k in keys:
-    hf.Module.kernel(P.source(args.form, P.MEMBERS[k].stem), grid=args.grid).run(img, args.grid)
+    hf.Module.kernel(P.source(args.form, P.MEMBERS[k].stem), grid=args.grid, specialize=img).run(img, args.grid)
 for p, d1 in pairs:
     a, b = p.split("+")
     m = hf.Module.fused(P.source(args.form, P.MEMBERS[a].stem), P.source(args.form, P.MEMBERS[b].stem),
-                        int(d1), 1024 - int(d1), grid=args.grid)
+                        int(d1), 1024 - int(d1), grid=args.grid, specialize=img)
     m.run(img, args.grid)
 import ctypes  # noqa: E402
 ctypes.CDLL("libcudart.so.12").cudaDeviceSynchronize()
