@@ -24,30 +24,24 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
   float avg; float m2; int n; float o_avg; float o_m2; int o_n; int tot; float fac; float delta;
   for (int c = blockIdx.x; c < bn_C; c = c + gridDim.x) {
     // Per-thread shifted sums (shift = the thread's first sample): s1 = sum(x - K),
-    // s2 = sum((x - K)^2), pairwise within each float4. Two float4 cursors per iteration
-    // (j and j + nthr of the flat N * HW/4 space) keep two 128-bit loads in flight.
+    // s2 = sum((x - K)^2), pairwise within each float4. Two float4 positions per iteration
+    // (j and j + nthr of the flat N * HW/4 space of channel c) keep two 128-bit loads in
+    // flight; plane/offset come from j / (HW/4) (a constant divisor once specialized).
     n = 0;
     float K = 0.0;
     float s1 = 0.0;
     float s2 = 0.0;
-    int b = 0;
-    int i = tid;
-    while (i >= hw4) {
-      i = i - hw4;
-      b = b + 1;
+    int total4 = bn_N * hw4;
+    if (tid < total4) {
+      int b0 = tid / hw4;
+      K = bn_x[((b0 * bn_C + c) * hw4 + tid - b0 * hw4) * 4];
     }
-    if (b < bn_N) {
-      K = bn_x[((b * bn_C + c) * hw4 + i) * 4];
-    }
-    while (b < bn_N) {
-      int i2 = i + nthr;
-      int b2 = b;
-      while (i2 >= hw4) {
-        i2 = i2 - hw4;
-        b2 = b2 + 1;
-      }
-      vload(bn_x, (b * bn_C + c) * hw4 + i, v0, v1, v2, v3);
-      vload(bn_x, (min(b2, bn_N - 1) * bn_C + c) * hw4 + i2, v4, v5, v6, v7);
+    for (int j = tid; j < total4; j = j + 2 * nthr) {
+      int j2 = min(j + nthr, total4 - 1);
+      int b = j / hw4;
+      int b2 = j2 / hw4;
+      vload(bn_x, (b * bn_C + c) * hw4 + j - b * hw4, v0, v1, v2, v3);
+      vload(bn_x, (b2 * bn_C + c) * hw4 + j2 - b2 * hw4, v4, v5, v6, v7);
       float e0 = v0 - K;
       float e1 = v1 - K;
       float e2 = v2 - K;
@@ -55,7 +49,7 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
       s1 = s1 + ((e0 + e1) + (e2 + e3));
       s2 = s2 + ((e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3));
       n = n + 4;
-      if (b2 < bn_N) {
+      if (j + nthr < total4) {
         e0 = v4 - K;
         e1 = v5 - K;
         e2 = v6 - K;
@@ -63,12 +57,6 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) d
         s1 = s1 + ((e0 + e1) + (e2 + e3));
         s2 = s2 + ((e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3));
         n = n + 4;
-      }
-      i = i2 + nthr;
-      b = b2;
-      while (i >= hw4) {
-        i = i - hw4;
-        b = b + 1;
       }
     }
     fac = 1.0 / fmaxf(1.0, n);
