@@ -7,6 +7,7 @@
 //                      [--granularity G] [--caps 32,40,...] [--reps N]
 //   hfuse occupancy [K] [--regs N --shmem B --threads T] [--sm S]
 //   hfuse check K              hfuse lower K [-o F]           hfuse emit K [-o F]
+//   hfuse profile CANDIDATE(.cu|.mk) --mem IMG... [--grid G]   (mkfuse --profiler-cmd target)
 //
 // Same flags, stdout keys and exit codes (0 ok; 1 + "error[Code] l:c: msg" on stderr).
 // `simulate` and `search` run on the GPU: the reference's cycle simulator is replaced by
@@ -191,7 +192,11 @@ int cmd_search(const Args& a) {
     if (!a.sm_given) sm = rt::sm_from_device();
     img = images(a);
     rt::upload(img);
-    be = std::make_unique<DeviceBackend>(img, a.grid, a.warmup, a.reps, true);
+    auto dev = std::make_unique<DeviceBackend>(img, a.grid, a.warmup, a.reps, true);
+    std::map<std::string, ScalarVal> spec;
+    for (const auto& [n, s] : img.scalars) spec[n] = ScalarVal{s.ty, s.i, s.f};
+    dev->set_specialization(spec);  // JIT-specialize every candidate to the image's shapes
+    be = std::move(dev);
   }
   SearchResult r = (n1.tunable && n2.tunable) ? search_config(n1, n2, a.d0, *be, sm, so)
                                               : fixed_partition_fuse(n1, n2, *be, sm, a.d0, so);
@@ -210,6 +215,78 @@ int cmd_search(const Args& a) {
     write_text(a.out, emit(r.best, st));
     std::printf("wrote %s\n", a.out.c_str());
   }
+  return 0;
+}
+
+// `hfuse profile CANDIDATE --mem IMG...`: the B200 profiler command for the reference's
+// ExternalCommandBackend (search.cpp:32-62). The candidate is the goto-style CUDA text (or
+// structured .mk) mkfuse writes as <fused>_<d1>_<regcap|0>_<n>.<ext>; the register cap is
+// recovered from that name. Prints the median device time in ns first (the "cycle count"
+// mkfuse reads), then `us = ...`.
+Sm100Kernel wrap_goto(const std::string& text, int grid) {
+  Sm100Kernel k;
+  size_t g = text.find("__global__ void ");
+  if (g == std::string::npos) raise(Code::InvalidArgument, "no __global__ kernel in the candidate");
+  size_t name_at = g + std::string("__global__ void ").size();
+  size_t lp = text.find('(', name_at), rp = text.find(')', lp);
+  k.entry = text.substr(name_at, lp - name_at);
+  std::stringstream ps(text.substr(lp + 1, rp - lp - 1));
+  std::string item;
+  while (std::getline(ps, item, ',')) {
+    std::stringstream is(item);
+    std::string type, name;
+    is >> type >> name;
+    if (type.empty()) continue;
+    bool array = type.back() == '*';
+    if (array) type.pop_back();
+    k.params.push_back(Sm100Param{name, type == "float" ? Ty::Float : Ty::Int, array, true});
+  }
+  auto size_of = [&](const char* key) {
+    size_t at = text.find(key);
+    if (at == std::string::npos) raise(Code::InvalidArgument, std::string("candidate has no ") + key);
+    return std::atoi(text.c_str() + at + std::strlen(key));
+  };
+  k.threads = size_of("size_1 = ") + size_of("size_2 = ");
+  k.grid = grid > 0 ? grid : 1;
+  k.source = text.substr(0, g) + "extern \"C\" " + text.substr(g);
+  return k;
+}
+
+int cmd_profile(const Args& a) {
+  need_inputs(a, 1);
+  if (!rt::device_available()) raise(Code::Device, "profile runs on the GPU; no CUDA device is visible");
+  std::filesystem::path path(a.inputs[0]);
+  std::string text = read_text(path.string());
+  Image img = images(a);
+  rt::upload(img);
+  std::optional<int> cap;
+  {
+    std::vector<std::string> parts;
+    std::stringstream ss(path.stem().string());
+    std::string p;
+    while (std::getline(ss, p, '_')) parts.push_back(p);
+    if (parts.size() >= 3) {
+      char* end = nullptr;
+      long v = std::strtol(parts[parts.size() - 2].c_str(), &end, 10);
+      if (end && *end == '\0' && v > 0) cap = int(v);
+    }
+  }
+  Sm100Kernel k;
+  if (path.extension() == ".mk") {
+    Loaded l = load_source(text, a.entry);
+    if (a.grid > 0) l.kernel.grid = a.grid;
+    if (!cap && l.kernel.regcap) cap = l.kernel.regcap;
+    Sm100Options o;
+    for (const auto& [n, s] : img.scalars) o.specialize[n] = ScalarVal{s.ty, s.i, s.f};
+    k = emit_sm100(l.kernel, l.prog.funcs, o);
+  } else {
+    k = wrap_goto(text, a.grid);
+  }
+  rt::Module m = rt::compile(k, cap);
+  rt::Timing t = rt::time(rt::Mode::Single, m, nullptr, img, a.grid, 0, a.warmup, a.reps, true);
+  std::printf("%lld\n", (long long)(t.median_us * 1000.0 + 0.5));
+  std::printf("us = %.3f\nregisters = %d\nblocks_per_sm = %d\n", t.median_us, m.regs, m.blocks_per_sm);
+  rt::unload(m);
   return 0;
 }
 
@@ -275,6 +352,7 @@ int main(int argc, char** argv) {
     if (a.cmd == "check") return cmd_check(a);
     if (a.cmd == "lower") return cmd_lower(a);
     if (a.cmd == "emit") return cmd_emit(a);
+    if (a.cmd == "profile") return cmd_profile(a);
     raise(Code::InvalidArgument, "unknown command '" + a.cmd + "'");
   } catch (const Error& e) {
     std::fprintf(stderr, "error%s\n", e.what());

@@ -1,0 +1,65 @@
+"""The CLI's device commands (simulate / search / profile) against the reference fixtures."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT, golden
+
+EXE = os.path.join(ROOT, "paper_2007_01277_b200", "bin", "hfuse")
+D = golden("corpus_digests.json")
+
+
+def write_corpus(corpus, tmp_path):
+    for stem, text in corpus["kernels"].items():
+        (tmp_path / f"{stem}.mk").write_text(text)
+    for stem, text in corpus["images"].items():
+        (tmp_path / f"{stem}.img").write_text(text)
+
+
+def run(*args):
+    return subprocess.run([EXE, *map(str, args)], capture_output=True, text=True, timeout=600)
+
+
+@pytest.mark.gpu
+def test_simulate_sequential_digest_matches_reference(gpu, corpus, tmp_path):
+    """`hfuse simulate --sequential` prints the same digest as `mkfuse simulate --sequential`."""
+    write_corpus(corpus, tmp_path)
+    rec = D["pairs"]["vector_add+strided_sum"]
+    r = run("simulate", "--sequential", tmp_path / "vector_add.mk", tmp_path / "strided_sum.mk",
+            "--mem", tmp_path / "vector_add.img", "--mem", tmp_path / "strided_sum.img", "--seed", 3)
+    assert r.returncode == 0, r.stderr
+    kv = dict(line.split(" = ") for line in r.stdout.strip().splitlines())
+    assert kv["digest"] == rec["seeds"]["3"]["sequential"]
+    assert float(kv["elapsed_us"]) > 0
+
+
+@pytest.mark.gpu
+def test_fused_structured_file_simulates_to_reference_digest(gpu, corpus, tmp_path):
+    write_corpus(corpus, tmp_path)
+    out = tmp_path / "f.mk"
+    assert run("fuse", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--d1", 896, "--d2", 128,
+               "--style", "structured", "-o", out).returncode == 0
+    r = run("simulate", out, "--mem", tmp_path / "batchnorm.img", "--mem", tmp_path / "histogram.img")
+    kv = dict(line.split(" = ") for line in r.stdout.strip().splitlines())
+    assert kv["digest"] == "d447034bfbccdc7c"  # proj/README.md:98,103
+
+
+@pytest.mark.gpu
+def test_search_on_device_and_profile_command(gpu, corpus, tmp_path):
+    write_corpus(corpus, tmp_path)
+    trace = tmp_path / "t.csv"
+    r = run("search", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--mem", tmp_path / "batchnorm.img",
+            "--mem", tmp_path / "histogram.img", "--trace", trace, "--reps", 3)
+    assert r.returncode == 0, r.stderr
+    assert "evaluated = 14" in r.stdout
+    rows = trace.read_text().splitlines()
+    assert rows[0] == "d1,d2,reg_cap,cycles,occupancy,utilization,us" and len(rows) == 15
+    # the reference's --profiler-cmd contract: goto candidate named <fused>_<d1>_<cap>_<n>.cu
+    cand = tmp_path / "fused_batchnorm_histogram_896_32_0.cu"
+    assert run("fuse", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--d1", 896, "--d2", 128,
+               "-o", cand).returncode == 0
+    p = run("profile", cand, "--mem", tmp_path / "batchnorm.img", "--mem", tmp_path / "histogram.img")
+    assert p.returncode == 0, p.stderr
+    first = p.stdout.split()[0]
+    assert first.isdigit() and int(first) > 0
