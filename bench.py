@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--search-reps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pairs", default="all")
+    ap.add_argument("--no-crypto", action="store_true", help="skip the C3/C4 crypto suite")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -357,6 +358,10 @@ def main():
 
     # ---- e2e: the same step through the C ABI from pinned host buffers
     e2e = e2e_step(hf, torch, P, pair_list, fused, work, keys, grid, stream, args)
+    del img  # free the DL images before the crypto suite (the Ethash DAG alone is 4 GiB)
+    crypto_res = None
+    if not args.no_crypto:
+        crypto_res = crypto_suite(hf, torch, args, rank, world, stream)
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -405,11 +410,91 @@ def main():
         "cpu_baseline": cpu,
         "setup_s": round(setup_s, 1),
         "search": {r["pair"]: r["search_trace"] for r in results},
+        "crypto": crypto_res,
     }
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+CRYPTO_COUNTS = {"sha256d": 1 << 24, "blake2b": 1 << 23, "blake256": 1 << 24, "ethash": 1 << 20}
+ETHASH_PAGES = 1 << 25  # 4 GiB synthetic DAG (>> the 126 MB L2)
+
+
+def crypto_suite(hf, torch, args, rank, world, stream):
+    """C3: SHA256d+Blake2B and Blake256+Ethash nonce search, nonce ranges sharded over ranks
+    (rank r owns [r * count, (r + 1) * count)), one reduction per pair (hit count sum, winning
+    nonce min); C4: Upsample (tunable) + Blake256 (fixed 512) over d0 in {640..1024} x
+    register caps {none, r0, 32, 40, 48, 64, 96}. Fused vs unfused under the flushed-L2 protocol."""
+    from paper_2007_01277_b200 import crypto as CR
+    from paper_2007_01277_b200 import pairs as P
+    grid = args.grid
+    srcs = {k: open(os.path.join(P.KERNELS, "b200", k + ".mk")).read() for k in CR.MEMBERS}
+    out = {"c3": [], "c4": None}
+    for a, b in (("sha256d", "blake2b"), ("blake256", "ethash")):
+        wa = CR.workload(a, CRYPTO_COUNTS[a], grid, nonce0=rank * CRYPTO_COUNTS[a], target=1 << 12)
+        wb = CR.workload(b, CRYPTO_COUNTS[b], grid, nonce0=rank * CRYPTO_COUNTS[b], target=1 << 12,
+                         npages=ETHASH_PAGES)
+        img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload(stream)
+        ka = hf.Module.kernel(srcs[a], grid=grid, specialize=img)
+        kb = hf.Module.kernel(srcs[b], grid=grid, specialize=img)
+        r = hf.search(srcs[a], srcs[b], img, grid=grid, reps=5, warmup=2, specialize=True)
+        m = hf.Module.fused(srcs[a], srcs[b], r["d1"], r["d2"], regcap=r["reg_cap"] or "off", grid=grid,
+                            specialize=img)
+        t = {mode: hf.time(mode, ka, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["median_us"]
+             for mode in ("sequential", "two_stream")}
+        tf = hf.time("single", m, None, img, grid, warmup=2, reps=10, stream=stream)["median_us"]
+        ta = hf.time("single", ka, None, img, grid, warmup=2, reps=10, stream=stream)["median_us"]
+        tb = hf.time("single", kb, None, img, grid, warmup=2, reps=10, stream=stream)["median_us"]
+        res = {"pair": f"{a}+{b}", "d1": r["d1"], "d2": r["d2"], "reg_cap": r["reg_cap"], "regs": m.info.regs,
+               "blocks_per_sm": m.info.blocks_per_sm, "a_us": ta, "b_us": tb, "seq_us": t["sequential"],
+               "two_stream_us": t["two_stream"], "fused_us": tf,
+               "speedup": min(t["sequential"], t["two_stream"]) / tf,
+               "nonces": {a: CRYPTO_COUNTS[a], b: CRYPTO_COUNTS[b]},
+               "mhash_s_fused": (CRYPTO_COUNTS[a] + CRYPTO_COUNTS[b]) / tf,
+               "search_trace": [(x["d1"], x["reg_cap"], round(x["us"], 1)) for x in r["trace"]]}
+        if b == "ethash":
+            res["dag_bytes"] = wb.dag_bytes
+            res["dag_gbs_fused"] = CRYPTO_COUNTS[b] * 64 * 128 / (tf * 1e3)
+        # the single exchange: total hits + winning nonce over all ranks
+        img_out = hf.Image(wa.image).merge(hf.Image(wb.image)).upload(stream)
+        m.run(img_out, grid, stream)
+        img_out.download(stream)
+        hits = torch.tensor([int(img_out.array(f"{CR.MEMBERS[k]}_cnt")[0]) for k in (a, b)], dtype=torch.int64)
+        win = torch.tensor([int(img_out.array(f"{CR.MEMBERS[k]}_bmin").min()) for k in (a, b)], dtype=torch.int64)
+        if world > 1:
+            import torch.distributed as dist
+            hits, win = hits.cuda(), win.cuda()
+            dist.all_reduce(hits)
+            dist.all_reduce(win, op=dist.ReduceOp.MIN)
+        res["hits"] = hits.tolist()
+        res["winning_nonce"] = win.tolist()
+        out["c3"].append(res)
+        del img, img_out
+    # C4: Upsample + Blake256
+    wu = P.MEMBERS["upsample"].sizes["full"](rank)
+    wb = CR.workload("blake256", 1 << 21, grid, nonce0=0, target=1 << 12)
+    img = hf.Image(wu.image).merge(hf.Image(wb.image)).upload(stream)
+    su = P.source("b200", "upsample")
+    ku = hf.Module.kernel(su, grid=grid, specialize=img)
+    kb = hf.Module.kernel(srcs["blake256"], grid=grid, specialize=img)
+    seq = hf.time("sequential", ku, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["median_us"]
+    two = hf.time("two_stream", ku, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["median_us"]
+    sweep = []
+    for d0 in (640, 768, 896, 1024):
+        try:
+            r = hf.search(su, srcs["blake256"], img, d0=d0, grid=grid, reps=5, warmup=2, specialize=True,
+                          extra_caps=(32, 40, 48, 64, 96))
+        except hf.HFuseError:
+            continue
+        for row in r["trace"]:
+            sweep.append({"d0": d0, "d1": row["d1"], "reg_cap": row["reg_cap"], "us": round(row["us"], 2),
+                          "occupancy": round(row["occupancy"], 3)})
+    best = min(sweep, key=lambda x: x["us"])
+    out["c4"] = {"pair": "upsample+blake256", "seq_us": seq, "two_stream_us": two, "best": best,
+                 "speedup": min(seq, two) / best["us"], "sweep": sweep}
+    return out
 
 
 def e2e_step(hf, torch, P, pair_list, fused, work, keys, grid, stream, args):

@@ -168,6 +168,11 @@ int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regca
 /* One unfused kernel at its declared dims (regcap: HF_REGCAP_OFF or a cap). */
 int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks,
                     const hf_image* specialize, hf_module** out, hf_error* err);
+/* The reference's naive goto emission (fuser.cpp:290-549) of the same pair, made launchable
+ * (extern "C", parameters from its signature) — the "naive fusion" baseline; its semantics
+ * are plain CUDA's, not the interpreter's, so it is timed, never parity-checked. */
+int hf_build_naive(const char* src1, const char* src2, int d1, int d2, int grid, hf_module** out,
+                   hf_error* err);
 int hf_module_get_info(const hf_module* m, hf_module_info* out);
 const char* hf_module_source(const hf_module* m);  /* borrowed */
 const char* hf_module_entry(const hf_module* m);   /* borrowed */

@@ -215,6 +215,15 @@ int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks, const
   });
 }
 
+int hf_build_naive(const char* src1, const char* src2, int d1, int d2, int grid, hf_module** out, hf_error* err) {
+  return guarded(err, [&] {
+    hf::FuseResult r = hf::fuse_sources(src1, src2, d1, d2, "off", hf::SM::b200());
+    auto h = std::make_unique<hf_module>();
+    h->m = hf::rt::compile(hf::wrap_goto(hf::emit_goto(r.fused), grid > 0 ? grid : r.fused.grid));
+    *out = h.release();
+  });
+}
+
 int hf_module_get_info(const hf_module* m, hf_module_info* out) {
   if (!m || !out) return to_abi(hf::Code::InvalidArgument);
   *out = hf_module_info{m->m.threads, m->m.grid, m->m.smem, m->m.regs, m->m.local_bytes, m->m.blocks_per_sm,

@@ -223,35 +223,6 @@ int cmd_search(const Args& a) {
 // structured .mk) mkfuse writes as <fused>_<d1>_<regcap|0>_<n>.<ext>; the register cap is
 // recovered from that name. Prints the median device time in ns first (the "cycle count"
 // mkfuse reads), then `us = ...`.
-Sm100Kernel wrap_goto(const std::string& text, int grid) {
-  Sm100Kernel k;
-  size_t g = text.find("__global__ void ");
-  if (g == std::string::npos) raise(Code::InvalidArgument, "no __global__ kernel in the candidate");
-  size_t name_at = g + std::string("__global__ void ").size();
-  size_t lp = text.find('(', name_at), rp = text.find(')', lp);
-  k.entry = text.substr(name_at, lp - name_at);
-  std::stringstream ps(text.substr(lp + 1, rp - lp - 1));
-  std::string item;
-  while (std::getline(ps, item, ',')) {
-    std::stringstream is(item);
-    std::string type, name;
-    is >> type >> name;
-    if (type.empty()) continue;
-    bool array = type.back() == '*';
-    if (array) type.pop_back();
-    k.params.push_back(Sm100Param{name, type == "float" ? Ty::Float : Ty::Int, array, true});
-  }
-  auto size_of = [&](const char* key) {
-    size_t at = text.find(key);
-    if (at == std::string::npos) raise(Code::InvalidArgument, std::string("candidate has no ") + key);
-    return std::atoi(text.c_str() + at + std::strlen(key));
-  };
-  k.threads = size_of("size_1 = ") + size_of("size_2 = ");
-  k.grid = grid > 0 ? grid : 1;
-  k.source = text.substr(0, g) + "extern \"C\" " + text.substr(g);
-  return k;
-}
-
 int cmd_profile(const Args& a) {
   need_inputs(a, 1);
   if (!rt::device_available()) raise(Code::Device, "profile runs on the GPU; no CUDA device is visible");

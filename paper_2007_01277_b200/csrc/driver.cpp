@@ -2,6 +2,7 @@
 
 #include <cstdio>
 #include <fstream>
+#include <cstring>
 #include <sstream>
 
 namespace hf {
@@ -85,6 +86,38 @@ std::string fuse_report(const FuseResult& r) {
   std::snprintf(buf, sizeof(buf), "occupancy_fraction = %.6f\n", occ.fraction);
   o += buf;
   return o;
+}
+
+// The reference's goto-style text (fuser.cpp:290-549) made launchable: `extern "C"` entry,
+// parameters parsed from the signature, block size from the prologue's size_1 + size_2.
+// Its semantics are the naive CUDA ones (not the interpreter's pinned ones): timing only.
+Sm100Kernel wrap_goto(const std::string& text, int grid) {
+  Sm100Kernel k;
+  size_t g = text.find("__global__ void ");
+  if (g == std::string::npos) raise(Code::InvalidArgument, "no __global__ kernel in the candidate");
+  size_t name_at = g + std::string("__global__ void ").size();
+  size_t lp = text.find('(', name_at), rp = text.find(')', lp);
+  k.entry = text.substr(name_at, lp - name_at);
+  std::stringstream ps(text.substr(lp + 1, rp - lp - 1));
+  std::string item;
+  while (std::getline(ps, item, ',')) {
+    std::stringstream is(item);
+    std::string type, name;
+    is >> type >> name;
+    if (type.empty()) continue;
+    bool array = type.back() == '*';
+    if (array) type.pop_back();
+    k.params.push_back(Sm100Param{name, type == "float" ? Ty::Float : Ty::Int, array, true, false, {}});
+  }
+  auto size_of = [&](const char* key) {
+    size_t at = text.find(key);
+    if (at == std::string::npos) raise(Code::InvalidArgument, std::string("candidate has no ") + key);
+    return std::atoi(text.c_str() + at + std::strlen(key));
+  };
+  k.threads = size_of("size_1 = ") + size_of("size_2 = ");
+  k.grid = grid > 0 ? grid : 1;
+  k.source = text.substr(0, g) + "extern \"C\" " + text.substr(g);
+  return k;
 }
 
 std::string emit(const Fused& f, Style style) {

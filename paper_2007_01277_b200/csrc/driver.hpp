@@ -30,5 +30,6 @@ FuseResult fuse_sources(const std::string& src1, const std::string& src2, int d1
 std::string fuse_report(const FuseResult& r);
 std::string emit(const Fused& f, Style style);
 std::string read_text(const std::string& path);
+Sm100Kernel wrap_goto(const std::string& goto_text, int grid);
 
 }  // namespace hf

@@ -815,10 +815,13 @@ class Parser {
           else if (b200() && n.text == "rotr") w = Intr::Rotr;
           else if (b200() && n.text == "rotl") w = Intr::Rotl;
           else if (b200() && n.text == "ltu") w = Intr::LtU;
+          else if (b200() && n.text == "fshr") w = Intr::Fshr;
+          else if (b200() && n.text == "fshl") w = Intr::Fshl;
           if (w) {
             std::vector<Expr> a = args();
             if (int(a.size()) != intr_arity(*w))
-              raise(Code::Syntax, n.text + " takes exactly two arguments", p);
+              raise(Code::Syntax, n.text + " takes exactly " +
+                                      std::string(intr_arity(*w) == 3 ? "three" : "two") + " arguments", p);
             e = intrin(*w, std::move(a));
             e.pos = p;
             return e;

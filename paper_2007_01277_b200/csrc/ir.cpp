@@ -36,11 +36,17 @@ const char* intr_name(Intr i) {
     case Intr::Rotr: return "rotr";
     case Intr::Rotl: return "rotl";
     case Intr::LtU: return "ltu";
+    case Intr::Fshr: return "fshr";
+    case Intr::Fshl: return "fshl";
   }
   return "?";
 }
 
-int intr_arity(Intr i) { return (i == Intr::CastInt || i == Intr::CastFloat) ? 1 : 2; }
+int intr_arity(Intr i) {
+  if (i == Intr::CastInt || i == Intr::CastFloat) return 1;
+  if (i == Intr::Fshr || i == Intr::Fshl) return 3;
+  return 2;
+}
 
 bool intr_is_extension(Intr i) { return int(i) >= int(Intr::ShrU); }
 

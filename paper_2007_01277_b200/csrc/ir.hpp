@@ -65,6 +65,8 @@ enum class Intr : uint8_t {
   Rotr,   // 32-bit rotate right
   Rotl,   // 32-bit rotate left
   LtU,    // unsigned less-than (0/1)
+  Fshr,   // fshr(lo, hi, n): low word of (hi:lo) >> (n & 31)   (64-bit rotates in 32-bit halves)
+  Fshl,   // fshl(lo, hi, n): high word of (hi:lo) << (n & 31)
 };
 const char* intr_name(Intr i);
 int intr_arity(Intr i);

@@ -642,7 +642,7 @@ struct Lowerer {
     for (auto& x : c.a) x = expr(x);
     if (c.k != EK::Intrin || !intr_is_extension(Intr(c.i))) return c;
     const Expr& x = c.a[0];
-    const Expr& n = c.a[1];
+    const Expr& n = c.a.size() > 1 ? c.a[1] : c.a[0];
     switch (Intr(c.i)) {
       case Intr::ShrU: return shr_u(x, n);
       case Intr::Rotr: {
@@ -661,6 +661,29 @@ struct Lowerer {
       }
       case Intr::LtU:
         return binary(Bin::Lt, binary(Bin::Xor, x, int_min()), binary(Bin::Xor, n, int_min()));
+      case Intr::Fshr:
+      case Intr::Fshl: {
+        // fshr(lo, hi, n) = n&31 == 0 ? lo : shr_u(lo, n) | hi << (32 - n)
+        // fshl(lo, hi, n) = n&31 == 0 ? hi : hi << n | shr_u(lo, 32 - n)
+        bool right = Intr(c.i) == Intr::Fshr;
+        const Expr& lo = c.a[0];
+        const Expr& hi = c.a[1];
+        const Expr& cnt = c.a[2];
+        if (auto k = const_of(cnt)) {
+          int s = *k & 31;
+          if (s == 0) return right ? lo : hi;
+          if (right) return binary(Bin::Or, shr_u(lo, lit(s)), binary(Bin::Shl, hi, lit(32 - s)));
+          return binary(Bin::Or, binary(Bin::Shl, hi, lit(s)), shr_u(lo, lit(32 - s)));
+        }
+        Expr s = binary(Bin::And, cnt, lit(31));
+        Expr back = binary(Bin::And, binary(Bin::Sub, lit(32), s), lit(31));
+        Expr mix = right ? binary(Bin::Or, shr_u(lo, s), binary(Bin::Shl, hi, back))
+                         : binary(Bin::Or, binary(Bin::Shl, hi, s), shr_u(lo, back));
+        Expr mask = unary(Un::Neg, binary(Bin::Ne, s, lit(0)));  // 0 or -1
+        Expr keep = right ? lo : hi;
+        return binary(Bin::Or, binary(Bin::And, keep, binary(Bin::Xor, mask, unary(Un::Neg, lit(1)))),
+                      binary(Bin::And, mix, mask));
+      }
       default: return c;
     }
   }

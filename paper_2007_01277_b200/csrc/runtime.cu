@@ -2,7 +2,7 @@
 //
 // * NVRTC compiles emitted kernels straight to an sm_100a CUBIN (no PTX JIT at load).
 // * Driver entry points come from cudaGetDriverEntryPoint so this library links only the
-//   static CUDA runtime + NVRTC and still loads on hosts without libcuda (CPU CI).
+//   CUDA runtime + NVRTC and still loads on hosts without libcuda (CPU CI).
 // * Memory images live in HBM; seeded arrays are generated on the device with the
 //   closed form of the reference's splitmix64 stream (memimage.cpp:10-61): element i of
 //   a seeded array is mix(seed + (i + 1) * golden), so every thread fills independently
@@ -12,7 +12,10 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <numeric>
 
@@ -174,6 +177,61 @@ SM sm_from_device(int device) {
   return sm;
 }
 
+namespace {
+// CUBIN cache keyed by FNV-1a of (source, options): the search re-emits identical candidates
+// (e.g. per-constituent register probes) and the bench rebuilds the winners. Optionally
+// persisted in $HFUSE_CACHE_DIR as <key>.cubin (SURVEY §5 checkpoint/resume row).
+std::mutex g_cache_mu;
+std::map<uint64_t, std::vector<char>> g_cache;
+
+uint64_t fnv(const std::string& s, uint64_t h = 14695981039346656037ULL) {
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+bool cache_get(uint64_t key, std::vector<char>& out) {
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {
+      out = it->second;
+      return true;
+    }
+  }
+  const char* dir = std::getenv("HFUSE_CACHE_DIR");
+  if (!dir) return false;
+  char name[64];
+  std::snprintf(name, sizeof(name), "/%016llx.cubin", (unsigned long long)key);
+  FILE* f = std::fopen((std::string(dir) + name).c_str(), "rb");
+  if (!f) return false;
+  std::fseek(f, 0, SEEK_END);
+  long n = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  out.resize(size_t(n));
+  bool ok = std::fread(out.data(), 1, size_t(n), f) == size_t(n);
+  std::fclose(f);
+  return ok;
+}
+
+void cache_put(uint64_t key, const std::vector<char>& cubin) {
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache[key] = cubin;
+  }
+  const char* dir = std::getenv("HFUSE_CACHE_DIR");
+  if (!dir) return;
+  char name[64];
+  std::snprintf(name, sizeof(name), "/%016llx.cubin", (unsigned long long)key);
+  if (FILE* f = std::fopen((std::string(dir) + name).c_str(), "wb")) {
+    std::fwrite(cubin.data(), 1, cubin.size(), f);
+    std::fclose(f);
+  }
+}
+}  // namespace
+
 Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) {
   Module m;
   m.entry = k.entry;
@@ -185,29 +243,34 @@ Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) 
   m.barriers = k.barriers;
   m.maxrreg = maxrreg;
 
-  nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, k.source.c_str(), (k.entry + ".cu").c_str(), 0, nullptr, nullptr) !=
-      NVRTC_SUCCESS)
-    raise(Code::Compile, "nvrtcCreateProgram failed");
   std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-fmad=false"};
   if (lineinfo) opts.push_back("-lineinfo");
   if (maxrreg) opts.push_back("--maxrregcount=" + std::to_string(*maxrreg));
-  std::vector<const char*> argv;
-  for (const auto& o : opts) argv.push_back(o.c_str());
-  nvrtcResult r = nvrtcCompileProgram(prog, int(argv.size()), argv.data());
-  size_t log_size = 0;
-  nvrtcGetProgramLogSize(prog, &log_size);
-  m.log.resize(log_size);
-  if (log_size) nvrtcGetProgramLog(prog, m.log.data());
-  if (r != NVRTC_SUCCESS) {
+  uint64_t key = fnv(k.entry, fnv(k.source));
+  for (const auto& o : opts) key = fnv(o, key);
+  if (!cache_get(key, m.cubin)) {
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, k.source.c_str(), (k.entry + ".cu").c_str(), 0, nullptr, nullptr) !=
+        NVRTC_SUCCESS)
+      raise(Code::Compile, "nvrtcCreateProgram failed");
+    std::vector<const char*> argv;
+    for (const auto& o : opts) argv.push_back(o.c_str());
+    nvrtcResult r = nvrtcCompileProgram(prog, int(argv.size()), argv.data());
+    size_t log_size = 0;
+    nvrtcGetProgramLogSize(prog, &log_size);
+    m.log.resize(log_size);
+    if (log_size) nvrtcGetProgramLog(prog, m.log.data());
+    if (r != NVRTC_SUCCESS) {
+      nvrtcDestroyProgram(&prog);
+      raise(Code::Compile, "NVRTC failed for '" + k.entry + "': " + m.log);
+    }
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    m.cubin.resize(n);
+    nvrtcGetCUBIN(prog, m.cubin.data());
     nvrtcDestroyProgram(&prog);
-    raise(Code::Compile, "NVRTC failed for '" + k.entry + "': " + m.log);
+    cache_put(key, m.cubin);
   }
-  size_t n = 0;
-  nvrtcGetCUBINSize(prog, &n);
-  m.cubin.resize(n);
-  nvrtcGetCUBIN(prog, m.cubin.data());
-  nvrtcDestroyProgram(&prog);
 
   if (!device_available()) return m;  // CPU hosts: compile-only (ptxas still ran)
   Driver& d = drv();

@@ -1,0 +1,514 @@
+"""Generator of the crypto member kernels (MK+), the C3/C4 workloads of SURVEY §8d.
+
+The paper's crypto kernels (ccminer SHA256d, Blake256, Blake2B and
+ethminer's Ethash) have fixed block sizes and straight-line, fully unrolled rounds. Mini-Kernel
+has no local arrays, so rounds are generated here as straight-line MK+ with statically
+renamed state registers (no register moves), hex constants, 32-bit rotates (funnel shifts on
+sm_100a) and 64-bit arithmetic in 32-bit halves (carry via `ltu`, rotates via `fshr`/`fshl`).
+Header words are scalar kernel parameters: they live in the constant bank, and with JIT
+specialization the nonce-independent first block (the midstate) folds at compile time.
+
+Common contract of every kernel (prefix P):
+  nonce of iteration n = P_nonce0 + n (32-bit wrap), n in [0, P_count), grid-stride;
+  P_cnt[0]  += number of nonces whose criterion word is below P_target (unsigned);
+  P_chk[0]  += digest word 0 (wrapping sum over all nonces);
+  P_bmin[b] = smallest hit nonce of block b (0x7fffffff if none).
+The Python restatement in oracle/crypto_ref.py (pinned on standard test vectors) computes the
+same three outputs.
+
+Run `python -m paper_2007_01277_b200.kernels.gen_crypto` to regenerate kernels/b200/*.mk.
+"""
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+SHA_K = [0x428A2F98, 0x71374491, 0xB5C0FBCF, 0xE9B5DBA5, 0x3956C25B, 0x59F111F1, 0x923F82A4, 0xAB1C5ED5,
+         0xD807AA98, 0x12835B01, 0x243185BE, 0x550C7DC3, 0x72BE5D74, 0x80DEB1FE, 0x9BDC06A7, 0xC19BF174,
+         0xE49B69C1, 0xEFBE4786, 0x0FC19DC6, 0x240CA1CC, 0x2DE92C6F, 0x4A7484AA, 0x5CB0A9DC, 0x76F988DA,
+         0x983E5152, 0xA831C66D, 0xB00327C8, 0xBF597FC7, 0xC6E00BF3, 0xD5A79147, 0x06CA6351, 0x14292967,
+         0x27B70A85, 0x2E1B2138, 0x4D2C6DFC, 0x53380D13, 0x650A7354, 0x766A0ABB, 0x81C2C92E, 0x92722C85,
+         0xA2BFE8A1, 0xA81A664B, 0xC24B8B70, 0xC76C51A3, 0xD192E819, 0xD6990624, 0xF40E3585, 0x106AA070,
+         0x19A4C116, 0x1E376C08, 0x2748774C, 0x34B0BCB5, 0x391C0CB3, 0x4ED8AA4A, 0x5B9CCA4F, 0x682E6FF3,
+         0x748F82EE, 0x78A5636F, 0x84C87814, 0x8CC70208, 0x90BEFFFA, 0xA4506CEB, 0xBEF9A3F7, 0xC67178F2]
+IV256 = [0x6A09E667, 0xBB67AE85, 0x3C6EF372, 0xA54FF53A, 0x510E527F, 0x9B05688C, 0x1F83D9AB, 0x5BE0CD19]
+B256_C = [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344, 0xA4093822, 0x299F31D0, 0x082EFA98, 0xEC4E6C89,
+          0x452821E6, 0x38D01377, 0xBE5466CF, 0x34E90C6C, 0xC0AC29B7, 0xC97C50DD, 0x3F84D5B5, 0xB5470917]
+SIGMA = [
+    [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15],
+    [14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3],
+    [11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4],
+    [7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8],
+    [9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13],
+    [2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9],
+    [12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11],
+    [13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10],
+    [6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5],
+    [10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0],
+]
+G_IDX = [(0, 4, 8, 12), (1, 5, 9, 13), (2, 6, 10, 14), (3, 7, 11, 15),
+         (0, 5, 10, 15), (1, 6, 11, 12), (2, 7, 8, 13), (3, 4, 9, 14)]
+IV512 = [0x6A09E667F3BCC908, 0xBB67AE8584CAA73B, 0x3C6EF372FE94F82B, 0xA54FF53A5F1D36F1,
+         0x510E527FADE682D1, 0x9B05688C2B3E6C1F, 0x1F83D9ABFB41BD6B, 0x5BE0CD19137E2179]
+RC = [0x0000000000000001, 0x0000000000008082, 0x800000000000808A, 0x8000000080008000, 0x000000000000808B,
+      0x0000000080000001, 0x8000000080008081, 0x8000000000008009, 0x000000000000008A, 0x0000000000000088,
+      0x0000000080008009, 0x000000008000000A, 0x000000008000808B, 0x800000000000008B, 0x8000000000008089,
+      0x8000000000008003, 0x8000000000008002, 0x8000000000000080, 0x000000000000800A, 0x800000008000000A,
+      0x8000000080008081, 0x8000000000008080, 0x0000000080000001, 0x8000000080008008]
+ROT = [[0, 36, 3, 41, 18], [1, 44, 10, 45, 2], [62, 6, 43, 15, 61], [28, 55, 25, 21, 56], [27, 20, 39, 8, 14]]
+
+
+def hx(v):
+    return f"0x{v & 0xFFFFFFFF:08x}"
+
+
+class Src:
+    def __init__(self):
+        self.lines = []
+        self.ind = 1
+
+    def __call__(self, s=""):
+        self.lines.append("  " * self.ind + s if s else "")
+
+    def text(self):
+        return "\n".join(self.lines) + "\n"
+
+
+def decls(src, names, ty="int"):
+    for i in range(0, len(names), 12):
+        src(" ".join(f"{ty} {n};" for n in names[i:i + 12]))
+
+
+def header(src, p, kind, doc, params, dims, shared=True):
+    src.lines.append(doc.rstrip())
+    src.lines.append("//@ grid=296")
+    src.lines.append(f"kernel {kind}({params}) dims ({dims}, 1, 1) fixed {{")
+    if shared:
+        src(f"shared int {p}_smin[32];")
+
+
+def tail(src, p):
+    """Per-block min of the hit nonces: 5-step shuffle tree, one smem stage, warp 0 folds."""
+    src(f"best = min(best, warp_shfl_xor(best, 16));")
+    src(f"best = min(best, warp_shfl_xor(best, 8));")
+    src(f"best = min(best, warp_shfl_xor(best, 4));")
+    src(f"best = min(best, warp_shfl_xor(best, 2));")
+    src(f"best = min(best, warp_shfl_xor(best, 1));")
+    src(f"if (tid % 32 == 0) {{")
+    src(f"  {p}_smin[tid / 32] = best;")
+    src("}")
+    src("syncthreads();")
+    src("if (tid < 32) {")
+    src(f"  best = 2147483647;")
+    src(f"  if (tid < nthr / 32) {{")
+    src(f"    best = {p}_smin[tid];")
+    src("  }")
+    for m in (16, 8, 4, 2, 1):
+        src(f"  best = min(best, warp_shfl_xor(best, {m}));")
+    src("  if (tid == 0) {")
+    src(f"    {p}_bmin[blockIdx.x] = best;")
+    src("  }")
+    src("}")
+    src.ind = 0
+    src("}")
+
+
+def loop_head(src, p):
+    src(f"int tid = threadIdx.x;")
+    src(f"int nthr = blockDim.x;")
+    src(f"int best = 2147483647;")
+    src(f"int cnt = 0;")
+    src(f"int chk = 0;")
+
+
+def loop_open(src, p):
+    src(f"for (int n = blockIdx.x * nthr + tid; n < {p}_count; n = n + gridDim.x * nthr) {{")
+    src.ind += 1
+    src(f"int nonce = {p}_nonce0 + n;")
+
+
+def loop_close(src, p, word, crit):
+    src(f"chk = chk + {word};")
+    src(f"if (ltu({crit}, {p}_target)) {{")
+    src("  cnt = cnt + 1;")
+    src("  best = min(best, nonce);")
+    src("}")
+    src.ind -= 1
+    src("}")
+    src(f"atomic_add({p}_chk[0], chk);")
+    src(f"if (cnt > 0) {{")
+    src(f"  atomic_add({p}_cnt[0], cnt);")
+    src("}")
+
+
+# ---------------------------------------------------------------------------------------
+# SHA-256d
+# ---------------------------------------------------------------------------------------
+
+def sha_rounds(src, roles, w, first_w=None):
+    """64 rounds; roles = list of 8 variable names (a..h); w = 16 schedule variable names.
+    Returns the final roles."""
+    R = list(roles)
+    for i in range(64):
+        if i >= 16:
+            x, x2, x7, x15 = w[i % 16], w[(i - 2) % 16], w[(i - 7) % 16], w[(i - 15) % 16]
+            src(f"{x} = (rotr({x2}, 17) ^ rotr({x2}, 19) ^ shr_u({x2}, 10)) + {x7} + "
+                f"(rotr({x15}, 7) ^ rotr({x15}, 18) ^ shr_u({x15}, 3)) + {x};")
+        a, b, c, d, e, f, g, h = R
+        src(f"t1 = {h} + (rotr({e}, 6) ^ rotr({e}, 11) ^ rotr({e}, 25)) + ({g} ^ ({e} & ({f} ^ {g}))) + "
+            f"{hx(SHA_K[i])} + {w[i % 16]};")
+        src(f"t2 = (rotr({a}, 2) ^ rotr({a}, 13) ^ rotr({a}, 22)) + (({a} & {b}) | ({c} & ({a} | {b})));")
+        src(f"{d} = {d} + t1;")
+        src(f"{h} = t1 + t2;")
+        R = [h, a, b, c, d, e, f, g]
+    return R
+
+
+def gen_sha256d():
+    p = "sh"
+    s = Src()
+    hp = ", ".join(f"int {p}_h{i}" for i in range(19))
+    header(s, p, "sha256d", """// SHA-256d nonce search (Bitcoin header hashing; ccminer sha256d analogue, PAPER.md:876).
+// Generated by kernels/gen_crypto.py. Header = 20 big-endian words (scalar params h0..h18,
+// word 19 = bswap(nonce)); digest = SHA256(SHA256(header)); criterion word = digest[7].
+// The nonce-independent first block (the midstate) is compressed once per thread.""",
+           f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], {hp}, int {p}_nonce0, int {p}_count, int {p}_target",
+           512)
+    st = [f"s{c}" for c in "abcdefgh"]
+    w = [f"w{i}" for i in range(16)]
+    mid = [f"m{i}" for i in range(8)]
+    dig = [f"d{i}" for i in range(8)]
+    decls(s, st + w + mid + dig + ["t1", "t2"])
+    loop_head(s, p)
+    for i in range(8):
+        s(f"{st[i]} = {hx(IV256[i])};")
+    for i in range(16):
+        s(f"{w[i]} = {p}_h{i};")
+    R = sha_rounds(s, st, w)
+    for i in range(8):
+        s(f"{mid[i]} = {hx(IV256[i])} + {R[i]};")
+    loop_open(s, p)
+    # block 2: header words 16..18, bswap(nonce), padding, length 640
+    s(f"w0 = {p}_h16;")
+    s(f"w1 = {p}_h17;")
+    s(f"w2 = {p}_h18;")
+    s("w3 = (nonce << 24) | ((nonce << 8) & 0x00ff0000) | (shr_u(nonce, 8) & 0x0000ff00) | shr_u(nonce, 24);")
+    s("w4 = 0x80000000;")
+    for i in range(5, 15):
+        s(f"w{i} = 0;")
+    s("w15 = 640;")
+    for i in range(8):
+        s(f"{st[i]} = {mid[i]};")
+    R = sha_rounds(s, st, w)
+    for i in range(8):
+        s(f"{dig[i]} = {mid[i]} + {R[i]};")
+    # second SHA-256 over the 32-byte digest
+    for i in range(8):
+        s(f"w{i} = {dig[i]};")
+    s("w8 = 0x80000000;")
+    for i in range(9, 15):
+        s(f"w{i} = 0;")
+    s("w15 = 256;")
+    for i in range(8):
+        s(f"{st[i]} = {hx(IV256[i])};")
+    R = sha_rounds(s, st, w)
+    for i in range(8):
+        s(f"{dig[i]} = {hx(IV256[i])} + {R[i]};")
+    loop_close(s, p, "d0", "d7")
+    tail(s, p)
+    return s.text()
+
+
+# ---------------------------------------------------------------------------------------
+# BLAKE-256 (14 rounds)
+# ---------------------------------------------------------------------------------------
+
+def blake256_compress(src, h, m, t, v):
+    """m: 16 expressions (variable names or hex literals); t: counter (python int)."""
+    for i in range(8):
+        src(f"{v[i]} = {h[i]};")
+    for i in range(4):
+        src(f"{v[8 + i]} = {hx(B256_C[i])};")
+    src(f"{v[12]} = {hx(t ^ B256_C[4])};")
+    src(f"{v[13]} = {hx(t ^ B256_C[5])};")
+    src(f"{v[14]} = {hx(B256_C[6])};")
+    src(f"{v[15]} = {hx(B256_C[7])};")
+    for r in range(14):
+        sg = SIGMA[r % 10]
+        for i, (a, b, c, d) in enumerate(G_IDX):
+            x, y = sg[2 * i], sg[2 * i + 1]
+            A, B, Cc, D = v[a], v[b], v[c], v[d]
+            src(f"{A} = {A} + {B} + ({m[x]} ^ {hx(B256_C[y])});")
+            src(f"{D} = rotr({D} ^ {A}, 16);")
+            src(f"{Cc} = {Cc} + {D};")
+            src(f"{B} = rotr({B} ^ {Cc}, 12);")
+            src(f"{A} = {A} + {B} + ({m[y]} ^ {hx(B256_C[x])});")
+            src(f"{D} = rotr({D} ^ {A}, 8);")
+            src(f"{Cc} = {Cc} + {D};")
+            src(f"{B} = rotr({B} ^ {Cc}, 7);")
+
+
+def gen_blake256():
+    p = "bl"
+    s = Src()
+    hp = ", ".join(f"int {p}_h{i}" for i in range(19))
+    header(s, p, "blake256", """// BLAKE-256 (14 rounds) nonce search (ccminer blake256 analogue, PAPER.md:876).
+// Generated by kernels/gen_crypto.py. Message = 80-byte header of big-endian words (scalar
+// params h0..h18, word 19 = nonce); two compressions (t = 512, t = 640); the first is
+// nonce-independent (midstate, once per thread). Criterion and checksum word = digest[0].""",
+           f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], {hp}, int {p}_nonce0, int {p}_count, int {p}_target",
+           512)
+    v = [f"v{i}" for i in range(16)]
+    mid = [f"m{i}" for i in range(8)]
+    decls(s, v + mid + ["h0", "h1", "h2", "h3", "h4", "h5", "h6", "h7"])
+    loop_head(s, p)
+    blake256_compress(s, [hx(x) for x in IV256], [f"{p}_h{i}" for i in range(16)], 512, v)
+    for i in range(8):
+        s(f"{mid[i]} = {hx(IV256[i])} ^ {v[i]} ^ {v[i + 8]};")
+    loop_open(s, p)
+    msg = [f"{p}_h16", f"{p}_h17", f"{p}_h18", "nonce", hx(0x80000000)] + ["0"] * 8 + ["1", "0", "640"]
+    blake256_compress(s, mid, msg, 640, v)
+    for i in range(8):
+        s(f"h{i} = {mid[i]} ^ {v[i]} ^ {v[i + 8]};")
+    loop_close(s, p, "h0", "h0")
+    tail(s, p)
+    return s.text()
+
+
+# ---------------------------------------------------------------------------------------
+# BLAKE2b-512 (64-bit lanes as 32-bit halves)
+# ---------------------------------------------------------------------------------------
+
+class Lane:
+    """A 64-bit value held in two 32-bit variables; swap() renames (rotr by 32 is free)."""
+
+    def __init__(self, lo, hi):
+        self.lo, self.hi = lo, hi
+
+
+def add64(src, a, b):
+    src(f"t = {a.lo} + {b.lo};")
+    src(f"{a.hi} = {a.hi} + {b.hi} + ltu(t, {a.lo});")
+    src(f"{a.lo} = t;")
+
+
+def add64_m(src, a, m):
+    """a += m where m = (lo_expr, hi_expr)."""
+    lo, hi = m
+    if lo == "0" and hi == "0":
+        return
+    src(f"t = {a.lo} + {lo};")
+    src(f"{a.hi} = {a.hi} + {hi} + ltu(t, {a.lo});")
+    src(f"{a.lo} = t;")
+
+
+def xor64(src, a, b):
+    src(f"{a.lo} = {a.lo} ^ {b.lo};")
+    src(f"{a.hi} = {a.hi} ^ {b.hi};")
+
+
+def rotr64(src, a, r):
+    if r == 32:
+        a.lo, a.hi = a.hi, a.lo
+        return
+    if r > 32:
+        a.lo, a.hi = a.hi, a.lo
+        r -= 32
+    src(f"t = fshr({a.lo}, {a.hi}, {r});")
+    src(f"{a.hi} = fshr({a.hi}, {a.lo}, {r});")
+    src(f"{a.lo} = t;")
+
+
+def gen_blake2b():
+    p = "b2"
+    s = Src()
+    hp = ", ".join(f"int {p}_h{i}" for i in range(19))
+    header(s, p, "blake2b", """// BLAKE2b-512 nonce search (ccminer blake2b analogue, PAPER.md:876).
+// Generated by kernels/gen_crypto.py. Message = 80-byte header of little-endian words
+// (scalar params h0..h18, word 19 = nonce): one compression with t = 80 and the final flag.
+// 64-bit lanes live in 32-bit halves: adds carry through ltu, rotates are funnel shifts
+// (SHF on sm_100a) and rotations by 32 are free renames. Criterion/checksum word = the low
+// 32 bits of digest lane 0.""",
+           f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], {hp}, int {p}_nonce0, int {p}_count, int {p}_target",
+           512)
+    names = []
+    for i in range(16):
+        names += [f"v{i}l", f"v{i}h"]
+    decls(s, names + ["t", "o0"])
+    loop_head(s, p)
+    loop_open(s, p)
+    words = [f"{p}_h{i}" for i in range(19)] + ["nonce"]
+    m = [(words[2 * k], words[2 * k + 1]) for k in range(10)] + [("0", "0")] * 6
+    v = [Lane(f"v{i}l", f"v{i}h") for i in range(16)]
+    h0 = list(IV512)
+    h0[0] ^= 0x01010040
+    for i in range(8):
+        s(f"{v[i].lo} = {hx(h0[i])};")
+        s(f"{v[i].hi} = {hx(h0[i] >> 32)};")
+    for i in range(8):
+        iv = IV512[i]
+        if i == 4:
+            iv ^= 80
+        if i == 6:
+            iv ^= 0xFFFFFFFFFFFFFFFF
+        s(f"{v[8 + i].lo} = {hx(iv)};")
+        s(f"{v[8 + i].hi} = {hx(iv >> 32)};")
+    for r in range(12):
+        sg = SIGMA[r % 10]
+        for i, (a, b, c, d) in enumerate(G_IDX):
+            A, B, Cc, D = v[a], v[b], v[c], v[d]
+            add64(s, A, B)
+            add64_m(s, A, m[sg[2 * i]])
+            xor64(s, D, A)
+            rotr64(s, D, 32)
+            add64(s, Cc, D)
+            xor64(s, B, Cc)
+            rotr64(s, B, 24)
+            add64(s, A, B)
+            add64_m(s, A, m[sg[2 * i + 1]])
+            xor64(s, D, A)
+            rotr64(s, D, 16)
+            add64(s, Cc, D)
+            xor64(s, B, Cc)
+            rotr64(s, B, 63)
+    s(f"o0 = {hx(h0[0])} ^ {v[0].lo} ^ {v[8].lo};")
+    loop_close(s, p, "o0", "o0")
+    tail(s, p)
+    return s.text()
+
+
+# ---------------------------------------------------------------------------------------
+# Ethash-style hashimoto: Keccak-512 seed, 64 DAG page mixes, Keccak-256 result
+# ---------------------------------------------------------------------------------------
+
+def keccak_f(src, A, rc_array):
+    """A: dict (x, y) -> Lane (current variable names). Emits the 24-round permutation as a
+    loop over one straight-line round (the round constants come from rc_array, 48 words)."""
+    C = [Lane(f"c{x}l", f"c{x}h") for x in range(5)]
+    D = Lane("dl", "dh")
+    src("for (int rnd = 0; rnd < 24; rnd = rnd + 1) {")
+    src.ind += 1
+    for x in range(5):
+        for half in ("lo", "hi"):
+            terms = " ^ ".join(getattr(A[(x, y)], half) for y in range(5))
+            src(f"{getattr(C[x], half)} = {terms};")
+    for x in range(5):
+        c1, c4 = C[(x + 1) % 5], C[(x - 1) % 5]
+        # D = C[x-1] ^ rotl64(C[x+1], 1)
+        src(f"{D.lo} = {c4.lo} ^ fshl({c1.hi}, {c1.lo}, 1);")
+        src(f"{D.hi} = {c4.hi} ^ fshl({c1.lo}, {c1.hi}, 1);")
+        for y in range(5):
+            src(f"{A[(x, y)].lo} = {A[(x, y)].lo} ^ {D.lo};")
+            src(f"{A[(x, y)].hi} = {A[(x, y)].hi} ^ {D.hi};")
+    # rho + pi into B (variables b{x}{y})
+    B = {}
+    for x in range(5):
+        for y in range(5):
+            r = ROT[x][y]
+            tx, ty = y, (2 * x + 3 * y) % 5
+            dst = Lane(f"b{tx}{ty}l", f"b{tx}{ty}h")
+            lo, hi = A[(x, y)].lo, A[(x, y)].hi
+            if r >= 32:
+                lo, hi = hi, lo
+                r -= 32
+            if r == 0:
+                src(f"{dst.lo} = {lo};")
+                src(f"{dst.hi} = {hi};")
+            else:
+                src(f"{dst.lo} = fshl({hi}, {lo}, {r});")
+                src(f"{dst.hi} = fshl({lo}, {hi}, {r});")
+            B[(tx, ty)] = dst
+    # chi back into A, iota from the round-constant table
+    for x in range(5):
+        for y in range(5):
+            b0, b1, b2 = B[(x, y)], B[((x + 1) % 5, y)], B[((x + 2) % 5, y)]
+            src(f"{A[(x, y)].lo} = {b0.lo} ^ (({b1.lo} ^ -1) & {b2.lo});")
+            src(f"{A[(x, y)].hi} = {b0.hi} ^ (({b1.hi} ^ -1) & {b2.hi});")
+    src(f"{A[(0, 0)].lo} = {A[(0, 0)].lo} ^ {rc_array}[rnd * 2];")
+    src(f"{A[(0, 0)].hi} = {A[(0, 0)].hi} ^ {rc_array}[rnd * 2 + 1];")
+    src.ind -= 1
+    src("}")
+
+
+def absorb_words(src, A, words):
+    """XOR 32-bit words (little-endian lane order) into the zero state: lane i = words[2i], [2i+1]."""
+    for i in range(25):
+        x, y = i % 5, i // 5
+        lo = words[2 * i] if 2 * i < len(words) else "0"
+        hi = words[2 * i + 1] if 2 * i + 1 < len(words) else "0"
+        src(f"{A[(x, y)].lo} = {lo};")
+        src(f"{A[(x, y)].hi} = {hi};")
+
+
+def gen_ethash():
+    p = "eh"
+    s = Src()
+    hp = ", ".join(f"int {p}_h{i}" for i in range(8))
+    header(s, p, "ethash", """// Ethash-style hashimoto nonce search (ethminer analogue, PAPER.md:876-879).
+// Generated by kernels/gen_crypto.py. seed = Keccak-512(header_hash[8 words] || nonce as
+// 64-bit LE); mix = seed repeated to 32 words; 64 rounds: page = fnv(i ^ seed[0],
+// mix[i % 32]) & (npages - 1), mix = fnv(mix, dag[page]) over the 128-byte page (eight
+// 128-bit loads); cmix = 8-word fnv fold; result = Keccak-256(seed || cmix).
+// Keccak-f[1600] lanes are 32-bit halves (rotates by funnel shifts, chi as LOP3); the 24
+// rounds are a loop over one straight-line round, round constants read from P_rc[48].
+// Criterion/checksum word = result word 0 (little-endian). The DAG is a synthetic
+// power-of-two page array (SURVEY §8d: a seeded int32 array, >= 4 GiB for C3).""",
+           f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], int {p}_dag[], int {p}_rc[], {hp}, int {p}_npages, "
+           f"int {p}_nonce0, int {p}_count, int {p}_target", 256)
+    A = {(x, y): Lane(f"a{x}{y}l", f"a{x}{y}h") for x in range(5) for y in range(5)}
+    names = []
+    for x in range(5):
+        for y in range(5):
+            names += [f"a{x}{y}l", f"a{x}{y}h", f"b{x}{y}l", f"b{x}{y}h"]
+    for x in range(5):
+        names += [f"c{x}l", f"c{x}h"]
+    names += ["dl", "dh"] + [f"sd{i}" for i in range(16)] + [f"mx{i}" for i in range(32)]
+    names += [f"cm{i}" for i in range(8)] + [f"q{i}" for i in range(32)] + ["pg", "r0"]
+    decls(s, names)
+    loop_head(s, p)
+    loop_open(s, p)
+    # Keccak-512: rate 72 bytes = 9 lanes; input 40 bytes = 10 words, pad 0x01 at byte 40,
+    # 0x80 at byte 71 (word 17, top byte)
+    words = [f"{p}_h{i}" for i in range(8)] + ["nonce", "0", "0x00000001"] + ["0"] * 6 + ["0x80000000"]
+    absorb_words(s, A, words)
+    keccak_f(s, A, f"{p}_rc")
+    for i in range(8):
+        ln = A[(i % 5, i // 5)]
+        s(f"sd{2 * i} = {ln.lo};")
+        s(f"sd{2 * i + 1} = {ln.hi};")
+    for i in range(32):
+        s(f"mx{i} = sd{i % 16};")
+    s(f"unroll for (int it = 0; it < 64; it = it + 32) {{")
+    s.ind += 1
+    for k in range(32):
+        s(f"pg = ((it + {k}) ^ sd0) * 16777619 ^ mx{k};")
+        s(f"pg = (pg & ({p}_npages - 1)) * 8;")
+        for j in range(8):
+            s(f"vload({p}_dag, pg + {j}, q{4 * j}, q{4 * j + 1}, q{4 * j + 2}, q{4 * j + 3});")
+        for j in range(32):
+            s(f"mx{j} = mx{j} * 16777619 ^ q{j};")
+    s.ind -= 1
+    s("}")
+    for k in range(8):
+        s(f"cm{k} = ((mx{4 * k} * 16777619 ^ mx{4 * k + 1}) * 16777619 ^ mx{4 * k + 2}) * 16777619 ^ mx{4 * k + 3};")
+    # Keccak-256: rate 136 bytes = 17 lanes; input 96 bytes = 24 words, pad 0x01 at byte 96,
+    # 0x80 at byte 135 (word 33, top byte)
+    words = [f"sd{i}" for i in range(16)] + [f"cm{i}" for i in range(8)] + ["0x00000001"] + ["0"] * 8 + ["0x80000000"]
+    absorb_words(s, A, words)
+    keccak_f(s, A, f"{p}_rc")
+    s(f"r0 = {A[(0, 0)].lo};")
+    loop_close(s, p, "r0", "r0")
+    tail(s, p)
+    return s.text()
+
+
+def main():
+    out = os.path.join(HERE, "b200")
+    for name, gen in (("sha256d", gen_sha256d), ("blake256", gen_blake256), ("blake2b", gen_blake2b),
+                      ("ethash", gen_ethash)):
+        with open(os.path.join(out, name + ".mk"), "w") as f:
+            f.write(gen())
+        print("wrote", name)
+
+
+if __name__ == "__main__":
+    main()

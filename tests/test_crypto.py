@@ -1,0 +1,110 @@
+"""Crypto members (C3/C4): the Python restatement is pinned on standard test vectors; the
+generated MK+ kernels (kernels/gen_crypto.py) run on the reference interpreter (after
+`hfuse lower`) and on the B200, and must reproduce the restatement's outputs exactly."""
+import os
+import struct
+import subprocess
+
+import pytest
+
+from oracle import crypto_ref as C
+from oracle import oracle
+from paper_2007_01277_b200 import crypto
+
+KERNELS = os.path.join(os.path.dirname(__file__), "..", "paper_2007_01277_b200", "kernels", "b200")
+KINDS = list(crypto.MEMBERS)
+
+
+def src(kind):
+    with open(os.path.join(KERNELS, kind + ".mk")) as f:
+        return f.read()
+
+
+def test_known_answer_vectors():
+    assert C.blake256(b"\x00").hex() == "0ce8d4ef4dd7cd8d62dfded9d4edb0a774ae6a41929a74da23109e8f11139c87"
+    assert C.blake256(b"\x00" * 72).hex() == "d419bad32d504fb7d44d460c42c5593fe544fa4c135dec31e21bd9abdcc22d41"
+    assert C.keccak256(b"").hex() == "c5d2460186f7233c927e7db2dcc703c0e500b653ca82273b7bfad8045d85a470"
+    assert C.keccak512(b"").hex().startswith("0eab42de4c3ceb9235fc91acffe746b29c29a8c366b7c60e4e67c466f36a4304")
+    words = list(struct.unpack(">20I", crypto.GENESIS_HEADER))
+    nonce = struct.unpack("<I", crypto.GENESIS_HEADER[76:80])[0]
+    d = C.sha256d_header(words, nonce)
+    assert b"".join(struct.pack(">I", x) for x in d)[::-1].hex() == \
+        "000000000019d6689c085ae165831e934ff763ae46a2a6c172b3f1b60a8ce26f"
+
+
+def test_generated_sources_are_current(tmp_path):
+    from paper_2007_01277_b200.kernels import gen_crypto
+    for kind, gen in (("sha256d", gen_crypto.gen_sha256d), ("blake256", gen_crypto.gen_blake256),
+                      ("blake2b", gen_crypto.gen_blake2b), ("ethash", gen_crypto.gen_ethash)):
+        assert gen() == src(kind), kind
+
+
+def reference_outputs(kind, count, grid, nonce0, target, words=None):
+    words = words or crypto.header_words(2024, 20)
+    dag = C.LazyDag(77, 1 << 10) if kind == "ethash" else None
+    return C.search_outputs(kind, words, nonce0, count, target, grid, crypto.THREADS[kind], dag=dag,
+                            n_pages=1 << 10)
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+@pytest.mark.parametrize("kind", KINDS)
+def test_lowered_kernels_on_reference_interpreter(hf, kind, tmp_path):
+    count, grid, nonce0, target = (6 if kind == "ethash" else 40), 1, 1000, 1 << 31
+    w = crypto.workload(kind, count=count, grid=grid, nonce0=nonce0, target=target)
+    (tmp_path / "k.mk").write_text(hf.lower(src(kind)))
+    (tmp_path / "k.img").write_text(w.image)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img", "--grid", grid)
+    arrays, _ = oracle.parse_image(dump)
+    p = crypto.MEMBERS[kind]
+    want = reference_outputs(kind, count, grid, nonce0, target)
+    assert int(arrays[f"{p}_cnt"][0]) == want["cnt"]
+    assert int(arrays[f"{p}_chk"][0]) == want["chk"]
+    assert [int(x) for x in arrays[f"{p}_bmin"]] == want["bmin"]
+
+
+def device_outputs(img, kind):
+    p = crypto.MEMBERS[kind]
+    return {"cnt": int(img.array(f"{p}_cnt")[0]), "chk": int(img.array(f"{p}_chk")[0]),
+            "bmin": [int(x) for x in img.array(f"{p}_bmin")]}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", KINDS)
+def test_crypto_member_on_device(gpu, kind):
+    hf = gpu
+    count, grid, nonce0, target = (512 if kind == "ethash" else 4096), 4, 77, 1 << 27
+    w = crypto.workload(kind, count=count, grid=grid, nonce0=nonce0, target=target)
+    img = hf.Image(w.image).upload()
+    hf.Module.kernel(src(kind), grid=grid, specialize=img).run(img, grid)
+    img.download()
+    assert device_outputs(img, kind) == reference_outputs(kind, count, grid, nonce0, target)
+
+
+@pytest.mark.gpu
+def test_sha256d_genesis_block_on_device(gpu):
+    hf = gpu
+    words = list(struct.unpack(">20I", crypto.GENESIS_HEADER))
+    nonce = struct.unpack("<I", crypto.GENESIS_HEADER[76:80])[0]  # 2083236893
+    w = crypto.workload("sha256d", count=1, grid=1, nonce0=nonce, target=1, words=words)
+    img = hf.Image(w.image).upload()
+    hf.Module.kernel(src("sha256d"), grid=1).run(img, 1)
+    img.download()
+    out = device_outputs(img, "sha256d")
+    assert out["cnt"] == 1 and out["bmin"] == [nonce]  # digest word 7 == 0: a valid block
+    assert out["chk"] == crypto.i32(0x6FE28C0A)  # first digest word of 000000000019d6...e26f
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("a,b", [("sha256d", "blake2b"), ("blake256", "ethash")])
+def test_fused_crypto_pairs_on_device(gpu, a, b):
+    hf = gpu
+    grid = 3
+    ca, cb = (2048, 2048) if b != "ethash" else (2048, 256)
+    wa = crypto.workload(a, count=ca, grid=grid, nonce0=5, target=1 << 28)
+    wb = crypto.workload(b, count=cb, grid=grid, nonce0=9, target=1 << 28)
+    img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
+    m = hf.Module.fused(src(a), src(b), crypto.THREADS[a], crypto.THREADS[b], grid=grid, specialize=img)
+    m.run(img, grid)
+    img.download()
+    assert device_outputs(img, a) == reference_outputs(a, ca, grid, 5, 1 << 28)
+    assert device_outputs(img, b) == reference_outputs(b, cb, grid, 9, 1 << 28)
