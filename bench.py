@@ -261,11 +261,19 @@ def main():
         two = hf.time("two_stream", unfused[a], unfused[b], img, grid, grid, warmup=2, reps=20, stream=stream)
         ta = hf.time("single", unfused[a], None, img, grid, warmup=2, reps=10, stream=stream)
         tb = hf.time("single", unfused[b], None, img, grid, warmup=2, reps=10, stream=stream)
+        # baselines of the paper's comparison: the reference's naive goto fusion of the naive
+        # member forms at the same split, and vertical fusion (VFuse) of the B200 forms
+        naive = hf.Module.naive(P.source("ref", P.MEMBERS[a].stem), P.source("ref", P.MEMBERS[b].stem),
+                                r["d1"], r["d2"], grid)
+        tn = hf.time("single", naive, None, img, grid, warmup=2, reps=10, stream=stream)
+        vert = hf.Module.vertical(src[a], src[b], grid, specialize=img)
+        tv = hf.time("single", vert, None, img, grid, warmup=2, reps=10, stream=stream)
         results.append({"pair": f"{a}+{b}", "d1": r["d1"], "d2": r["d2"], "reg_cap": cap,
                         "bytes": work[a].bytes + work[b].bytes, "regs": m.info.regs,
                         "blocks_per_sm": m.info.blocks_per_sm, "fused_us": fz["median_us"],
                         "seq_us": seq["median_us"], "two_stream_us": two["median_us"],
                         "a_us": ta["median_us"], "b_us": tb["median_us"],
+                        "naive_fused_us": tn["median_us"], "vertical_us": tv["median_us"],
                         "search_trace": [(t["d1"], t["reg_cap"], round(t["us"], 2)) for t in r["trace"]]})
     setup_s = time.perf_counter() - t_setup
 

@@ -173,6 +173,11 @@ int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks,
  * are plain CUDA's, not the interpreter's, so it is timed, never parity-checked. */
 int hf_build_naive(const char* src1, const char* src2, int d1, int d2, int grid, hf_module** out,
                    hf_error* err);
+/* Vertical fusion (VFuse; reference test-local version test_sim.cpp:398-439):
+ * both bodies run back to back by every thread of one block (equal block dims required);
+ * pinned semantics like hf_build_kernel. */
+int hf_build_vertical(const char* src1, const char* src2, int grid, const hf_image* specialize,
+                      hf_module** out, hf_error* err);
 int hf_module_get_info(const hf_module* m, hf_module_info* out);
 const char* hf_module_source(const hf_module* m);  /* borrowed */
 const char* hf_module_entry(const hf_module* m);   /* borrowed */

@@ -224,6 +224,21 @@ int hf_build_naive(const char* src1, const char* src2, int d1, int d2, int grid,
   });
 }
 
+int hf_build_vertical(const char* src1, const char* src2, int grid, const hf_image* specialize, hf_module** out,
+                      hf_error* err) {
+  return guarded(err, [&] {
+    hf::Loaded l1 = hf::load_source(src1), l2 = hf::load_source(src2);
+    hf::Kernel v = hf::vertical_fuse(hf::normalize(l1.kernel, l1.prog.funcs, "k1_"),
+                                     hf::normalize(l2.kernel, l2.prog.funcs, "k2_"));
+    if (grid > 0) v.grid = grid;
+    hf::Sm100Options o;
+    o.specialize = scalars_of(specialize);
+    auto h = std::make_unique<hf_module>();
+    h->m = hf::rt::compile(hf::emit_sm100(v, {}, o));
+    *out = h.release();
+  });
+}
+
 int hf_module_get_info(const hf_module* m, hf_module_info* out) {
   if (!m || !out) return to_abi(hf::Code::InvalidArgument);
   *out = hf_module_info{m->m.threads, m->m.grid, m->m.smem, m->m.regs, m->m.local_bytes, m->m.blocks_per_sm,

@@ -272,6 +272,62 @@ Fused fuse(const Kernel& k1, const Kernel& k2, int d1, int d2, const SM& sm) {
   return f;
 }
 
+// Vertical fusion (VFuse, the paper's comparison point PAPER.md:889-890; the reference keeps
+// only a test-local version, test_sim.cpp:398-439): same block, every thread runs k1's body
+// then k2's body. Returns of k1 jump to the end of k1's body so k2 still runs.
+Kernel vertical_fuse(const Kernel& k1, const Kernel& k2) {
+  require_normalized(k1);
+  require_normalized(k2);
+  if (!(k1.dims == k2.dims))
+    raise(Code::DimensionMismatch, "vertical fusion needs equal block dims ('" + k1.name + "' vs '" +
+                                       k2.name + "')");
+  if (k1.grid != k2.grid)
+    raise(Code::GridMismatch, "grid dimensions differ: '" + k1.name + "' uses " + std::to_string(k1.grid) +
+                                  ", '" + k2.name + "' uses " + std::to_string(k2.grid));
+  Kernel v;
+  v.name = "vertical_" + k1.name + "_" + k2.name;
+  v.dims = k1.dims;
+  v.tunable = false;
+  v.grid = k1.grid;
+  v.params = k1.params;
+  for (const auto& p : k2.params) {
+    auto it = std::find_if(v.params.begin(), v.params.end(), [&](const Param& q) { return q.name == p.name; });
+    if (it == v.params.end()) v.params.push_back(p);
+    else if (it->ty != p.ty || it->array != p.array)
+      raise(Code::TypeMismatch, "parameter '" + p.name + "' has conflicting types across the two kernels");
+  }
+  v.shared = k1.shared;
+  for (const auto& sh : k2.shared) v.shared.push_back(sh);
+  Block d1, r1, d2, r2;
+  auto split = [](const Kernel& k, Block& d, Block& r) {
+    size_t i = 0;
+    while (i < k.body.size() && k.body[i].k == SK::Decl) d.push_back(k.body[i++]);
+    for (; i < k.body.size(); ++i) r.push_back(k.body[i]);
+  };
+  split(k1, d1, r1);
+  split(k2, d2, r2);
+  bool returns = false;
+  walk(r1, [&](Stmt& s) {
+    if (s.k == SK::Return) {
+      s.k = SK::Goto;
+      s.name = "vf_k1_end";
+      s.val.clear();
+      returns = true;
+    }
+  });
+  for (auto& s : d1) v.body.push_back(s);
+  for (auto& s : d2) v.body.push_back(s);
+  for (auto& s : r1) v.body.push_back(s);
+  if (returns) {
+    Stmt l;
+    l.k = SK::Label;
+    l.name = "vf_k1_end";
+    v.body.push_back(l);
+  }
+  for (auto& s : r2) v.body.push_back(s);
+  return v;
+}
+
 Kernel Fused::to_kernel() const {
   Kernel k;
   k.name = name;

@@ -93,6 +93,7 @@ Block build_prologue(Dims dims1, Dims dims2, int d1);
 Block rewrite_builtins(const Block& body);
 Block replace_barriers(const Block& body, int id, int count);
 Fused fuse(const Kernel& k1, const Kernel& k2, int d1, int d2, const SM& sm);
+Kernel vertical_fuse(const Kernel& k1, const Kernel& k2);  // VFuse baseline (normalized inputs)
 Dims partition_dims(const Kernel& k, int d);
 
 enum class Style { Structured, Goto, Sm100 };

@@ -38,7 +38,8 @@ TIME_MODES = {"single": 0, "sequential": 1, "two_stream": 2}
 EXPORTS = [
     "hf_free", "hf_version", "hf_fuse", "hf_fuse_report", "hf_normalize", "hf_check", "hf_lower",
     "hf_emit_kernel", "hf_register_bound", "hf_occupancy", "hf_device_count",
-    "hf_get_device_props", "hf_build_fused", "hf_build_kernel", "hf_build_naive", "hf_module_get_info",
+    "hf_get_device_props", "hf_build_fused", "hf_build_kernel", "hf_build_naive", "hf_build_vertical",
+    "hf_module_get_info",
     "hf_module_source", "hf_module_entry", "hf_module_param", "hf_module_barrier",
     "hf_module_cubin", "hf_launch", "hf_module_free", "hf_image_parse", "hf_image_merge",
     "hf_image_materialize", "hf_image_upload", "hf_image_download", "hf_image_digest",
@@ -123,6 +124,7 @@ def _load() -> C.CDLL:
         "hf_build_fused": (ip, [cp, cp, ip, ip, ip, ip, ip, vp, C.POINTER(vp), E]),
         "hf_build_kernel": (ip, [cp, ip, ip, ip, vp, C.POINTER(vp), E]),
         "hf_build_naive": (ip, [cp, cp, ip, ip, ip, C.POINTER(vp), E]),
+        "hf_build_vertical": (ip, [cp, cp, ip, vp, C.POINTER(vp), E]),
         "hf_module_get_info": (ip, [vp, C.POINTER(_ModInfo)]),
         "hf_module_source": (cp, [vp]),
         "hf_module_entry": (cp, [vp]),
@@ -413,6 +415,14 @@ class Module:
         """The reference's goto-style fusion text compiled as-is (timing baseline only)."""
         h, err = C.c_void_p(), _Err()
         _check(_lib.hf_build_naive(src1.encode(), src2.encode(), d1, d2, grid, C.byref(h), C.byref(err)), err)
+        return cls(h)
+
+    @classmethod
+    def vertical(cls, src1: str, src2: str, grid: int = 0, specialize: Optional["Image"] = None) -> "Module":
+        """VFuse: both bodies back to back in one block (equal block dims)."""
+        h, err = C.c_void_p(), _Err()
+        _check(_lib.hf_build_vertical(src1.encode(), src2.encode(), grid, specialize._h if specialize else None,
+                                      C.byref(h), C.byref(err)), err)
         return cls(h)
 
     @property

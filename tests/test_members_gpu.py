@@ -115,3 +115,27 @@ def test_full_size_fused_pair_matches_c_oracle(gpu, pair):
     img.download()
     check_full(a, img)
     check_full(b, img)
+
+
+@pytest.mark.gpu
+def test_vertical_fusion_matches_sequential_interpreter(gpu):
+    """VFuse of two thread-count-independent members reproduces the sequential digest."""
+    hf = gpu
+    sa, sb = pairs.source("b200", "histogram"), pairs.source("b200", "maxpool")
+    img = image(hf, "hist", "maxpool").upload()
+    hf.Module.vertical(sa, sb, grid=GRID, specialize=img).run(img, GRID)
+    img.download()
+    assert img.digest_hex() == G["pairs"]["hist+maxpool"]["512"]["digest"]
+
+
+@pytest.mark.gpu
+def test_naive_goto_fusion_runs(gpu):
+    """The reference's goto text of the naive forms compiles and runs on sm_100a (timing
+    baseline); on these inputs it also computes the right histogram."""
+    hf = gpu
+    m = hf.Module.naive(pairs.source("ref", "batchnorm"), pairs.source("ref", "histogram"), 512, 512, grid=GRID)
+    img = image(hf, "bn", "hist").upload()
+    m.run(img, GRID)
+    img.download()
+    want = G["members"]["hist"]["parity"]["ref"]["outputs"]["hi_out"]
+    assert [int(x) for x in img.array("hi_out").view(np.uint32)] == want
