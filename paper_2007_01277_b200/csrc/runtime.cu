@@ -245,12 +245,24 @@ Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) 
 
   std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-fmad=false"};
   if (lineinfo) opts.push_back("-lineinfo");
-  if (maxrreg) opts.push_back("--maxrregcount=" + std::to_string(*maxrreg));
-  uint64_t key = fnv(k.entry, fnv(k.source));
+  std::string source = k.source;
+  if (maxrreg) {
+    // --maxrregcount is ignored for kernels that carry __launch_bounds__, so a register cap
+    // replaces the emitted launch bounds with __maxnreg__ (the two cannot be combined).
+    size_t at = source.find("__launch_bounds__(");
+    if (at != std::string::npos) {
+      size_t end = source.find(')', at);
+      source.replace(at, end - at + 1, "__maxnreg__(" + std::to_string(*maxrreg) + ")");
+    } else {
+      opts.push_back("--maxrregcount=" + std::to_string(*maxrreg));
+    }
+  }
+  m.source = source;
+  uint64_t key = fnv(k.entry, fnv(source));
   for (const auto& o : opts) key = fnv(o, key);
   if (!cache_get(key, m.cubin)) {
     nvrtcProgram prog;
-    if (nvrtcCreateProgram(&prog, k.source.c_str(), (k.entry + ".cu").c_str(), 0, nullptr, nullptr) !=
+    if (nvrtcCreateProgram(&prog, source.c_str(), (k.entry + ".cu").c_str(), 0, nullptr, nullptr) !=
         NVRTC_SUCCESS)
       raise(Code::Compile, "nvrtcCreateProgram failed");
     std::vector<const char*> argv;

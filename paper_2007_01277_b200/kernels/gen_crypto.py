@@ -439,6 +439,17 @@ def absorb_words(src, A, words):
         src(f"{A[(x, y)].hi} = {hi};")
 
 
+def bcast8(src, var, lane_src, tmp="bt"):
+    """Broadcast `var` from group lane `lane_src` (0..7, static or a variable) to the 8 lanes of each
+    8-lane group with a 3-step xor butterfly: at step m a lane whose bit m differs from the
+    source's adopts its partner's value (lj = lane % 8)."""
+    for m in (1, 2, 4):
+        src(f"{tmp} = warp_shfl_xor({var}, {m});")
+        src(f"if (((lj ^ {lane_src}) & {m}) != 0) {{")
+        src(f"  {var} = {tmp};")
+        src("}")
+
+
 def gen_ethash():
     p = "eh"
     s = Src()
@@ -446,10 +457,15 @@ def gen_ethash():
     header(s, p, "ethash", """// Ethash-style hashimoto nonce search (ethminer analogue, PAPER.md:876-879).
 // Generated by kernels/gen_crypto.py. seed = Keccak-512(header_hash[8 words] || nonce as
 // 64-bit LE); mix = seed repeated to 32 words; 64 rounds: page = fnv(i ^ seed[0],
-// mix[i % 32]) & (npages - 1), mix = fnv(mix, dag[page]) over the 128-byte page (eight
-// 128-bit loads); cmix = 8-word fnv fold; result = Keccak-256(seed || cmix).
-// Keccak-f[1600] lanes are 32-bit halves (rotates by funnel shifts, chi as LOP3); the 24
-// rounds are a loop over one straight-line round, round constants read from P_rc[48].
+// mix[i % 32]) & (npages - 1), mix = fnv(mix, dag[page]) over the 128-byte page;
+// cmix = 8-word fnv fold; result = Keccak-256(seed || cmix).
+// B200 mechanics (ethminer's lane-cooperative layout): every thread computes the two Keccaks
+// of its own nonce, but the DAG loop of the 8 nonces of an 8-lane group is shared: lane j
+// holds words 4j..4j+3 of all 8 mixes, the lane owning mix[i % 32] computes each page index
+// and broadcasts it (xor-butterfly shuffles), and each DAG page is read by the 8 lanes as
+// one coalesced 128-byte segment (8 pages per round in flight per lane, 4 lines per warp
+// load instead of 32). Keccak-f[1600] lanes are 32-bit halves (funnel-shift rotates, chi as
+// LOP3), 24 rounds as a loop over one straight-line round (constants from P_rc[48]).
 // Criterion/checksum word = result word 0 (little-endian). The DAG is a synthetic
 // power-of-two page array (SURVEY §8d: a seeded int32 array, >= 4 GiB for C3).""",
            f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], int {p}_dag[], int {p}_rc[], {hp}, int {p}_npages, "
@@ -461,11 +477,21 @@ def gen_ethash():
             names += [f"a{x}{y}l", f"a{x}{y}h", f"b{x}{y}l", f"b{x}{y}h"]
     for x in range(5):
         names += [f"c{x}l", f"c{x}h"]
-    names += ["dl", "dh"] + [f"sd{i}" for i in range(16)] + [f"mx{i}" for i in range(32)]
-    names += [f"cm{i}" for i in range(8)] + [f"q{i}" for i in range(32)] + ["pg", "r0"]
+    names += ["dl", "dh"] + [f"sd{i}" for i in range(16)] + [f"cm{i}" for i in range(8)]
+    names += [f"x{h}_{k}" for h in range(8) for k in range(4)] + [f"z{h}" for h in range(8)]
+    names += [f"pg{h}" for h in range(8)] + ["q0", "q1", "q2", "q3", "bt", "bw", "cw", "r0", "lj", "valid", "nonce"]
     decls(s, names)
-    loop_head(s, p)
-    loop_open(s, p)
+    s("int tid = threadIdx.x;")
+    s("int nthr = blockDim.x;")
+    s("int best = 2147483647;")
+    s("int cnt = 0;")
+    s("int chk = 0;")
+    s("int lane = tid % 32;")
+    s("lj = lane % 8;")
+    s(f"for (int n0 = blockIdx.x * nthr + (tid / 32) * 32; n0 < {p}_count; n0 = n0 + gridDim.x * nthr) {{")
+    s.ind += 1
+    s("valid = n0 + lane < " + f"{p}_count;")
+    s(f"nonce = {p}_nonce0 + n0 + lane;")
     # Keccak-512: rate 72 bytes = 9 lanes; input 40 bytes = 10 words, pad 0x01 at byte 40,
     # 0x80 at byte 71 (word 17, top byte)
     words = [f"{p}_h{i}" for i in range(8)] + ["nonce", "0", "0x00000001"] + ["0"] * 6 + ["0x80000000"]
@@ -475,28 +501,58 @@ def gen_ethash():
         ln = A[(i % 5, i // 5)]
         s(f"sd{2 * i} = {ln.lo};")
         s(f"sd{2 * i + 1} = {ln.hi};")
-    for i in range(32):
-        s(f"mx{i} = sd{i % 16};")
-    s(f"unroll for (int it = 0; it < 64; it = it + 32) {{")
+    # mixes of the group's 8 nonces: lane j keeps words 4j..4j+3 (= seed words 4(j % 4)..)
+    for h in range(8):
+        for w in range(16):
+            s(f"bw = sd{w};")
+            bcast8(s, "bw", h)
+            if w == 0:
+                s(f"z{h} = bw;")
+            s(f"if (lj % 4 == {w // 4}) {{")
+            s(f"  x{h}_{w % 4} = bw;")
+            s("}")
+    s("for (int it = 0; it < 64; it = it + 4) {")
     s.ind += 1
-    for k in range(32):
-        s(f"pg = ((it + {k}) ^ sd0) * 16777619 ^ mx{k};")
-        s(f"pg = (pg & ({p}_npages - 1)) * 8;")
-        for j in range(8):
-            s(f"vload({p}_dag, pg + {j}, q{4 * j}, q{4 * j + 1}, q{4 * j + 2}, q{4 * j + 3});")
-        for j in range(32):
-            s(f"mx{j} = mx{j} * 16777619 ^ q{j};")
+    s("int owner = (it % 32) / 4;")
+    for k in range(4):
+        for h in range(8):
+            s(f"pg{h} = ((it + {k}) ^ z{h}) * 16777619 ^ x{h}_{k};")
+            bcast8(s, f"pg{h}", "owner")
+            s(f"pg{h} = (pg{h} & ({p}_npages - 1)) * 8 + lj;")
+        for h in range(8):
+            s(f"vload({p}_dag, pg{h}, q0, q1, q2, q3);")
+            for j in range(4):
+                s(f"x{h}_{j} = x{h}_{j} * 16777619 ^ q{j};")
     s.ind -= 1
     s("}")
-    for k in range(8):
-        s(f"cm{k} = ((mx{4 * k} * 16777619 ^ mx{4 * k + 1}) * 16777619 ^ mx{4 * k + 2}) * 16777619 ^ mx{4 * k + 3};")
+    # cmix word j of nonce h sits in lane j; transpose so each lane holds its own nonce's 8 words
+    for h in range(8):
+        s(f"cw = ((x{h}_0 * 16777619 ^ x{h}_1) * 16777619 ^ x{h}_2) * 16777619 ^ x{h}_3;")
+        for k in range(8):
+            s("bw = cw;")
+            bcast8(s, "bw", k)
+            s(f"if (lj == {h}) {{")
+            s(f"  cm{k} = bw;")
+            s("}")
     # Keccak-256: rate 136 bytes = 17 lanes; input 96 bytes = 24 words, pad 0x01 at byte 96,
     # 0x80 at byte 135 (word 33, top byte)
     words = [f"sd{i}" for i in range(16)] + [f"cm{i}" for i in range(8)] + ["0x00000001"] + ["0"] * 8 + ["0x80000000"]
     absorb_words(s, A, words)
     keccak_f(s, A, f"{p}_rc")
     s(f"r0 = {A[(0, 0)].lo};")
-    loop_close(s, p, "r0", "r0")
+    s("if (valid) {")
+    s("  chk = chk + r0;")
+    s(f"  if (ltu(r0, {p}_target)) {{")
+    s("    cnt = cnt + 1;")
+    s("    best = min(best, nonce);")
+    s("  }")
+    s("}")
+    s.ind -= 1
+    s("}")
+    s(f"atomic_add({p}_chk[0], chk);")
+    s("if (cnt > 0) {")
+    s(f"  atomic_add({p}_cnt[0], cnt);")
+    s("}")
     tail(s, p)
     return s.text()
 
