@@ -54,6 +54,7 @@ RC = [0x0000000000000001, 0x0000000000008082, 0x800000000000808A, 0x800000008000
       0x0000000080008009, 0x000000008000000A, 0x000000008000808B, 0x800000000000008B, 0x8000000000008089,
       0x8000000000008003, 0x8000000000008002, 0x8000000000000080, 0x000000000000800A, 0x800000008000000A,
       0x8000000080008081, 0x8000000000008080, 0x0000000080000001, 0x8000000080008008]
+HPP = 4  # Ethash: nonces of an 8-lane group whose DAG walks are in flight together per lane
 ROT = [[0, 36, 3, 41, 18], [1, 44, 10, 45, 2], [62, 6, 43, 15, 61], [28, 55, 25, 21, 56], [27, 20, 39, 8, 14]]
 
 
@@ -78,10 +79,10 @@ def decls(src, names, ty="int"):
         src(" ".join(f"{ty} {n};" for n in names[i:i + 12]))
 
 
-def header(src, p, kind, doc, params, dims, shared=True):
+def header(src, p, kind, doc, params, dims, shared=True, fixed=True):
     src.lines.append(doc.rstrip())
     src.lines.append("//@ grid=296")
-    src.lines.append(f"kernel {kind}({params}) dims ({dims}, 1, 1) fixed {{")
+    src.lines.append(f"kernel {kind}({params}) dims ({dims}, 1, 1){' fixed' if fixed else ''} {{")
     if shared:
         src(f"shared int {p}_smin[32];")
 
@@ -380,9 +381,27 @@ def gen_blake2b():
 # Ethash-style hashimoto: Keccak-512 seed, 64 DAG page mixes, Keccak-256 result
 # ---------------------------------------------------------------------------------------
 
+PI_CYCLE = [(1, 0), (0, 2), (2, 1), (1, 2), (2, 3), (3, 3), (3, 0), (0, 1), (1, 3), (3, 1), (1, 4), (4, 4),
+            (4, 0), (0, 3), (3, 4), (4, 3), (3, 2), (2, 2), (2, 0), (0, 4), (4, 2), (2, 4), (4, 1), (1, 1)]
+
+
+def rotl64_into(src, dst_lo, dst_hi, lo, hi, r):
+    if r >= 32:
+        lo, hi = hi, lo
+        r -= 32
+    if r == 0:
+        src(f"{dst_lo} = {lo};")
+        src(f"{dst_hi} = {hi};")
+    else:
+        src(f"{dst_lo} = fshl({hi}, {lo}, {r});")
+        src(f"{dst_hi} = fshl({lo}, {hi}, {r});")
+
+
 def keccak_f(src, A, rc_array):
     """A: dict (x, y) -> Lane (current variable names). Emits the 24-round permutation as a
-    loop over one straight-line round (the round constants come from rc_array, 48 words)."""
+    loop over one straight-line, low-register round: theta with 5 column parities, rho+pi in
+    place along the 24-lane pi cycle (one carried lane), chi row by row (5 saved lanes); the
+    round constants come from rc_array (48 words)."""
     C = [Lane(f"c{x}l", f"c{x}h") for x in range(5)]
     D = Lane("dl", "dh")
     src("for (int rnd = 0; rnd < 24; rnd = rnd + 1) {")
@@ -399,30 +418,28 @@ def keccak_f(src, A, rc_array):
         for y in range(5):
             src(f"{A[(x, y)].lo} = {A[(x, y)].lo} ^ {D.lo};")
             src(f"{A[(x, y)].hi} = {A[(x, y)].hi} ^ {D.hi};")
-    # rho + pi into B (variables b{x}{y})
-    B = {}
-    for x in range(5):
-        for y in range(5):
-            r = ROT[x][y]
-            tx, ty = y, (2 * x + 3 * y) % 5
-            dst = Lane(f"b{tx}{ty}l", f"b{tx}{ty}h")
-            lo, hi = A[(x, y)].lo, A[(x, y)].hi
-            if r >= 32:
-                lo, hi = hi, lo
-                r -= 32
-            if r == 0:
-                src(f"{dst.lo} = {lo};")
-                src(f"{dst.hi} = {hi};")
-            else:
-                src(f"{dst.lo} = fshl({hi}, {lo}, {r});")
-                src(f"{dst.hi} = fshl({lo}, {hi}, {r});")
-            B[(tx, ty)] = dst
-    # chi back into A, iota from the round-constant table
-    for x in range(5):
-        for y in range(5):
-            b0, b1, b2 = B[(x, y)], B[((x + 1) % 5, y)], B[((x + 2) % 5, y)]
-            src(f"{A[(x, y)].lo} = {b0.lo} ^ (({b1.lo} ^ -1) & {b2.lo});")
-            src(f"{A[(x, y)].hi} = {b0.hi} ^ (({b1.hi} ^ -1) & {b2.hi});")
+    # rho + pi in place: the lane at p moves to pi(p) = (y, 2x + 3y) rotated by ROT[p]
+    src(f"tl = {A[PI_CYCLE[0]].lo};")
+    src(f"th = {A[PI_CYCLE[0]].hi};")
+    for i, pos in enumerate(PI_CYCLE):
+        dst = PI_CYCLE[(i + 1) % 24]
+        x, y = pos
+        if i < 23:
+            src(f"ul = {A[dst].lo};")
+            src(f"uh = {A[dst].hi};")
+        rotl64_into(src, A[dst].lo, A[dst].hi, "tl", "th", ROT[x][y])
+        if i < 23:
+            src("tl = ul;")
+            src("th = uh;")
+    # chi row by row, iota from the round-constant table
+    for y in range(5):
+        for x in range(5):
+            src(f"{C[x].lo} = {A[(x, y)].lo};")
+            src(f"{C[x].hi} = {A[(x, y)].hi};")
+        for x in range(5):
+            b1, b2 = C[(x + 1) % 5], C[(x + 2) % 5]
+            src(f"{A[(x, y)].lo} = {C[x].lo} ^ (({b1.lo} ^ -1) & {b2.lo});")
+            src(f"{A[(x, y)].hi} = {C[x].hi} ^ (({b1.hi} ^ -1) & {b2.hi});")
     src(f"{A[(0, 0)].lo} = {A[(0, 0)].lo} ^ {rc_array}[rnd * 2];")
     src(f"{A[(0, 0)].hi} = {A[(0, 0)].hi} ^ {rc_array}[rnd * 2 + 1];")
     src.ind -= 1
@@ -461,25 +478,28 @@ def gen_ethash():
 // cmix = 8-word fnv fold; result = Keccak-256(seed || cmix).
 // B200 mechanics (ethminer's lane-cooperative layout): every thread computes the two Keccaks
 // of its own nonce, but the DAG loop of the 8 nonces of an 8-lane group is shared: lane j
-// holds words 4j..4j+3 of all 8 mixes, the lane owning mix[i % 32] computes each page index
-// and broadcasts it (xor-butterfly shuffles), and each DAG page is read by the 8 lanes as
-// one coalesced 128-byte segment (8 pages per round in flight per lane, 4 lines per warp
-// load instead of 32). Keccak-f[1600] lanes are 32-bit halves (funnel-shift rotates, chi as
-// LOP3), 24 rounds as a loop over one straight-line round (constants from P_rc[48]).
+// holds words 4j..4j+3 of 4 of the group's mixes at a time, the lane owning mix[i % 32]
+// computes each page index and broadcasts it (xor-butterfly shuffles), and each DAG page is
+// read by the 8 lanes as one coalesced 128-byte segment (4 pages in flight per lane per
+// round, 4 lines per warp load instead of 32). Keccak-f[1600] lanes are 32-bit halves (funnel-shift rotates, chi as
+// LOP3, rho+pi in place along the pi cycle, chi row by row: ~64 live registers), 24 rounds as
+// a loop over one straight-line round (constants from P_rc[48]).
 // Criterion/checksum word = result word 0 (little-endian). The DAG is a synthetic
-// power-of-two page array (SURVEY §8d: a seeded int32 array, >= 4 GiB for C3).""",
+// power-of-two page array (SURVEY §8d: a seeded int32 array, >= 4 GiB for C3). Any warp-
+// multiple block size works (tunable: the partition search sizes it against its partner).""",
            f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], int {p}_dag[], int {p}_rc[], {hp}, int {p}_npages, "
-           f"int {p}_nonce0, int {p}_count, int {p}_target", 256)
+           f"int {p}_nonce0, int {p}_count, int {p}_target", 256, fixed=False)
     A = {(x, y): Lane(f"a{x}{y}l", f"a{x}{y}h") for x in range(5) for y in range(5)}
     names = []
     for x in range(5):
         for y in range(5):
-            names += [f"a{x}{y}l", f"a{x}{y}h", f"b{x}{y}l", f"b{x}{y}h"]
+            names += [f"a{x}{y}l", f"a{x}{y}h"]
     for x in range(5):
         names += [f"c{x}l", f"c{x}h"]
     names += ["dl", "dh"] + [f"sd{i}" for i in range(16)] + [f"cm{i}" for i in range(8)]
-    names += [f"x{h}_{k}" for h in range(8) for k in range(4)] + [f"z{h}" for h in range(8)]
-    names += [f"pg{h}" for h in range(8)] + ["q0", "q1", "q2", "q3", "bt", "bw", "cw", "r0", "lj", "valid", "nonce"]
+    names += [f"x{h}_{k}" for h in range(HPP) for k in range(4)] + [f"z{h}" for h in range(HPP)]
+    names += [f"pg{h}" for h in range(HPP)] + ["q0", "q1", "q2", "q3", "bt", "bw", "cw", "r0", "lj", "valid", "nonce"]
+    names += ["tl", "th", "ul", "uh"]
     decls(s, names)
     s("int tid = threadIdx.x;")
     s("int nthr = blockDim.x;")
@@ -501,11 +521,14 @@ def gen_ethash():
         ln = A[(i % 5, i // 5)]
         s(f"sd{2 * i} = {ln.lo};")
         s(f"sd{2 * i + 1} = {ln.hi};")
-    # mixes of the group's 8 nonces: lane j keeps words 4j..4j+3 (= seed words 4(j % 4)..)
-    for h in range(8):
+    # The group's 8 nonces are processed HPP at a time: lane j keeps words 4j..4j+3 of the
+    # mixes of nonces hg .. hg+HPP-1 (= seed words 4(j % 4) .. of those nonces).
+    s(f"for (int hg = 0; hg < 8; hg = hg + {HPP}) {{")
+    s.ind += 1
+    for h in range(HPP):
         for w in range(16):
             s(f"bw = sd{w};")
-            bcast8(s, "bw", h)
+            bcast8(s, "bw", f"(hg + {h})")
             if w == 0:
                 s(f"z{h} = bw;")
             s(f"if (lj % 4 == {w // 4}) {{")
@@ -515,25 +538,27 @@ def gen_ethash():
     s.ind += 1
     s("int owner = (it % 32) / 4;")
     for k in range(4):
-        for h in range(8):
+        for h in range(HPP):
             s(f"pg{h} = ((it + {k}) ^ z{h}) * 16777619 ^ x{h}_{k};")
             bcast8(s, f"pg{h}", "owner")
             s(f"pg{h} = (pg{h} & ({p}_npages - 1)) * 8 + lj;")
-        for h in range(8):
+        for h in range(HPP):
             s(f"vload({p}_dag, pg{h}, q0, q1, q2, q3);")
             for j in range(4):
                 s(f"x{h}_{j} = x{h}_{j} * 16777619 ^ q{j};")
     s.ind -= 1
     s("}")
-    # cmix word j of nonce h sits in lane j; transpose so each lane holds its own nonce's 8 words
-    for h in range(8):
+    # cmix word j of nonce hg+h sits in lane j; transpose so each lane keeps its own nonce's
+    for h in range(HPP):
         s(f"cw = ((x{h}_0 * 16777619 ^ x{h}_1) * 16777619 ^ x{h}_2) * 16777619 ^ x{h}_3;")
         for k in range(8):
             s("bw = cw;")
             bcast8(s, "bw", k)
-            s(f"if (lj == {h}) {{")
+            s(f"if (lj == hg + {h}) {{")
             s(f"  cm{k} = bw;")
             s("}")
+    s.ind -= 1
+    s("}")
     # Keccak-256: rate 136 bytes = 17 lanes; input 96 bytes = 24 words, pad 0x01 at byte 96,
     # 0x80 at byte 135 (word 33, top byte)
     words = [f"sd{i}" for i in range(16)] + [f"cm{i}" for i in range(8)] + ["0x00000001"] + ["0"] * 8 + ["0x80000000"]
