@@ -334,6 +334,8 @@ def main():
             unfused[a].run(img, grid, stream)
             unfused[b].run(img, grid, side)
             stream.wait_stream(side)
+        if dist is not None:
+            reduce_outputs()
 
     with ClockSampler(local) as clocks:
         for _ in range(args.warmup):
@@ -398,6 +400,9 @@ def main():
             traffic = None
 
     if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
         return 0
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -438,8 +443,9 @@ def main():
         "search": {r["pair"]: r["search_trace"] for r in results},
         "crypto": crypto_res,
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     if dist is not None:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 
