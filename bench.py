@@ -34,7 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fused-pair speedup vs max(sequential, 2-stream) unfused, µs; %roofline at 1/8 B200"
-SAMPLE_DIV = 256  # CPU baseline sample = 1/256 of each member's workload
+SAMPLE_DIV = 32  # CPU baseline sample = 1/32 of each member's workload (~10-30 s of CPU work per step)
 
 
 def load_peaks():
@@ -50,20 +50,21 @@ def load_peaks():
 # CPU reference: the reference interpreter (oracle/_ref) on a bounded sample
 # ---------------------------------------------------------------------------------------
 
-def sample_images():
-    """Per-member sample images: 1/SAMPLE_DIV of the full workload along the batch/channel axis."""
+def sample_images(div=SAMPLE_DIV):
+    """Per-member sample images: 1/div of the full workload along the batch/channel axis."""
+    C, n, mp, us, ic = 256 // div, 51380224 // div, 4096 // div, 16384 // div, 2048 // div
     return {
-        "bn": ("array bn_x float32 200704 seed 1 uniform -1 1\narray bn_stats float32 2 zero\n"
-               "scalar bn_N int32 64\nscalar bn_C int32 1\nscalar bn_HW int32 3136\n"),
-        "hist": "array hi_x float32 200704 seed 2 uniform -4 4\narray hi_out int32 64 zero\nscalar hi_n int32 200704\n",
-        "maxpool": ("array mp_x float32 200704 seed 3 uniform -1 1\narray mp_y float32 50176 zero\n"
-                    "array mp_idx int32 50176 zero\nscalar mp_NC int32 16\nscalar mp_H int32 112\n"
+        "bn": (f"array bn_x float32 {64 * C * 3136} seed 1 uniform -1 1\narray bn_stats float32 {2 * C} zero\n"
+               f"scalar bn_N int32 64\nscalar bn_C int32 {C}\nscalar bn_HW int32 3136\n"),
+        "hist": f"array hi_x float32 {n} seed 2 uniform -4 4\narray hi_out int32 64 zero\nscalar hi_n int32 {n}\n",
+        "maxpool": (f"array mp_x float32 {mp * 112 * 112} seed 3 uniform -1 1\narray mp_y float32 {mp * 56 * 56} zero\n"
+                    f"array mp_idx int32 {mp * 56 * 56} zero\nscalar mp_NC int32 {mp}\nscalar mp_H int32 112\n"
                     "scalar mp_W int32 112\nscalar mp_OH int32 56\nscalar mp_OW int32 56\n"),
-        "upsample": ("array us_x float32 50176 seed 4 uniform -1 1\narray us_y float32 200704 zero\n"
-                     "scalar us_NC int32 64\nscalar us_IH int32 28\nscalar us_IW int32 28\n"
+        "upsample": (f"array us_x float32 {us * 28 * 28} seed 4 uniform -1 1\narray us_y float32 {us * 56 * 56} zero\n"
+                     f"scalar us_NC int32 {us}\nscalar us_IH int32 28\nscalar us_IW int32 28\n"
                      "scalar us_OH int32 56\nscalar us_OW int32 56\n"),
-        "im2col": ("array ic_x float32 25088 seed 5 uniform -1 1\narray ic_col float32 225792 zero\n"
-                   "scalar ic_NC int32 8\nscalar ic_H int32 56\nscalar ic_W int32 56\n"),
+        "im2col": (f"array ic_x float32 {ic * 56 * 56} seed 5 uniform -1 1\narray ic_col float32 {ic * 9 * 56 * 56} zero\n"
+                   f"scalar ic_NC int32 {ic}\nscalar ic_H int32 56\nscalar ic_W int32 56\n"),
     }
 
 
@@ -112,13 +113,14 @@ def cpu_baseline(pairs_mod, steps=1):
         # port: the C restatement, multi-threaded
         import numpy as np
         t0 = time.perf_counter()
-        x = oracle.fill_uniform(200704, 1, -1.0, 1.0)
+        n = 51380224 // SAMPLE_DIV
+        x = oracle.fill_uniform(n, 1, -1.0, 1.0)
         for _ in range(4):
-            oracle.bn_stats(x, 64, 1, 3136)
+            oracle.bn_stats(x, 64, 256 // SAMPLE_DIV, 3136)
             oracle.hist(x)
-            oracle.maxpool(x, 16, 112, 112)
-            oracle.upsample(x[:50176], 64, 28, 28)
-            oracle.im2col(x[:25088], 8, 56, 56)
+            oracle.maxpool(x, 4096 // SAMPLE_DIV, 112, 112)
+            oracle.upsample(x[:n // 4], 16384 // SAMPLE_DIV, 28, 28)
+            oracle.im2col(x[:n // 8], 2048 // SAMPLE_DIV, 56, 56)
         wall = time.perf_counter() - t0
         del np
         return {"value": wall * SAMPLE_DIV * 1e6, "unit": "us", "cores": oracle.threads(), "kind": "port",
@@ -146,7 +148,7 @@ def run_reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32/int32", "data": "synthetic (seeded splitmix64)",
         "config": {"workload": "C2: 10 DL pairs (BN, Hist, Im2Col, MaxPool, Upsample), naive member forms, "
-                               "sequential run_functional, extrapolated from a 1/256 sample",
+                               f"sequential run_functional, extrapolated from a 1/{SAMPLE_DIV} sample",
                    "sample_div": SAMPLE_DIV},
         "cpu_baseline": {"value": us, "unit": "us", "cores": cores, "kind": "reference",
                          "sample": f"mkfuse_ref seq on 1/{SAMPLE_DIV} of each member, 10 pairs over {cores} processes"},
@@ -288,10 +290,10 @@ def main():
         tv = hf.time("single", vert, None, img, grid, warmup=2, reps=10, stream=stream)
         results.append({"pair": f"{a}+{b}", "d1": r["d1"], "d2": r["d2"], "reg_cap": cap,
                         "bytes": work[a].bytes + work[b].bytes, "regs": m.info.regs,
-                        "blocks_per_sm": m.info.blocks_per_sm, "fused_us": fz["median_us"],
-                        "seq_us": seq["median_us"], "two_stream_us": two["median_us"],
-                        "a_us": ta["median_us"], "b_us": tb["median_us"],
-                        "naive_fused_us": tn["median_us"], "vertical_us": tv["median_us"],
+                        "blocks_per_sm": m.info.blocks_per_sm, "fused_us": fz["iqm_us"],
+                        "seq_us": seq["iqm_us"], "two_stream_us": two["iqm_us"],
+                        "a_us": ta["iqm_us"], "b_us": tb["iqm_us"],
+                        "naive_fused_us": tn["iqm_us"], "vertical_us": tv["iqm_us"],
                         "search_trace": [(t["d1"], t["reg_cap"], round(t["us"], 2)) for t in r["trace"]]})
     setup_s = time.perf_counter() - t_setup
 
@@ -388,8 +390,10 @@ def main():
     e2e = e2e_step(hf, torch, P, pair_list, fused, work, keys, grid, stream, args)
     del img  # free the DL images before the crypto suite (the Ethash DAG alone is 4 GiB)
     crypto_res = None
+    clk = clocks.summary()
     if not args.no_crypto:
-        crypto_res = crypto_suite(hf, torch, args, rank, world, stream)
+        crypto_res = crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=clk.get("sm_mhz"),
+                                  hbm_peak=hbm_peak)
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -437,7 +441,7 @@ def main():
                      "peak_source": peak_src, "algorithmic_bytes": dom["bytes"]},
         "e2e": e2e,
         "gpu_launches": len(pair_list) * args.steps,
-        "clocks": clocks.summary(),
+        "clocks": clk,
         "cpu_baseline": cpu,
         "setup_s": round(setup_s, 1),
         "search": {r["pair"]: r["search_trace"] for r in results},
@@ -454,7 +458,32 @@ CRYPTO_COUNTS = {"sha256d": 1 << 24, "blake2b": 1 << 23, "blake256": 1 << 24, "e
 ETHASH_PAGES = 1 << 25  # 4 GiB synthetic DAG (>> the 126 MB L2)
 
 
-def crypto_suite(hf, torch, args, rank, world, stream):
+def crypto_roofline(nonces, t_us, sm_mhz, hbm_peak):
+    """Pair roofline of SURVEY.md §8d: max(issue time, HBM time). Issue time = warp
+    instructions / (148 SMs x 4 schedulers x f_sm), with each member's warp instructions per
+    nonce measured once by ncu (scripts/ncu_crypto_inst.py -> profiles/crypto_inst.json; SHA-256d
+    and the BLAKEs are data-independent, Ethash's page walk is fixed at 64 accesses). HBM time:
+    Ethash reads 64 pages x 128 B per nonce. Also the ALU-pipe bound (16 lanes per scheduler:
+    2 cycles per warp ALU instruction), the tighter ceiling for the rotate/xor-heavy hashes."""
+    path = os.path.join(ROOT, "profiles", "crypto_inst.json")
+    if not os.path.exists(path) or not sm_mhz:
+        return None
+    table = json.load(open(path))
+    if any(k not in table for k in nonces):
+        return None
+    slots = 148 * 4 * sm_mhz * 1e6
+    winst = sum(n * table[k]["warp_inst_per_nonce"] for k, n in nonces.items())
+    alu = sum(n * table[k]["alu_warp_inst_per_nonce"] for k, n in nonces.items())
+    t_issue = winst / slots * 1e6
+    t_alu = 2 * alu / slots * 1e6
+    t_hbm = sum(n * 64 * 128 for k, n in nonces.items() if k == "ethash") / (hbm_peak * 1e3)
+    t_roof = max(t_issue, t_hbm)
+    return {"bound": "issue" if t_issue >= t_hbm else "hbm", "roofline_us": t_roof, "frac": t_roof / t_us,
+            "issue_us": t_issue, "alu_pipe_us": t_alu, "alu_frac": t_alu / t_us, "hbm_us": t_hbm,
+            "warp_inst": winst, "sm_mhz": sm_mhz}
+
+
+def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=6557.4):
     """C3: SHA256d+Blake2B and Blake256+Ethash nonce search, nonce ranges sharded over ranks
     (rank r owns [r * count, (r + 1) * count)), one reduction per pair (hit count sum, winning
     nonce min); C4: Upsample (tunable) + Blake256 (fixed 512) over d0 in {640..1024} x
@@ -486,11 +515,11 @@ def crypto_suite(hf, torch, args, rank, world, stream):
         r = best_r
         m = hf.Module.fused(srcs[a], srcs[b], r["d1"], r["d2"], regcap=r["reg_cap"] or "off", grid=grid,
                             specialize=img)
-        t = {mode: hf.time(mode, ka, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["median_us"]
+        t = {mode: hf.time(mode, ka, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
              for mode in ("sequential", "two_stream")}
-        tf = hf.time("single", m, None, img, grid, warmup=2, reps=10, stream=stream)["median_us"]
-        ta = hf.time("single", ka, None, img, grid, warmup=2, reps=10, stream=stream)["median_us"]
-        tb = hf.time("single", kb, None, img, grid, warmup=2, reps=10, stream=stream)["median_us"]
+        tf = hf.time("single", m, None, img, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
+        ta = hf.time("single", ka, None, img, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
+        tb = hf.time("single", kb, None, img, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
         res = {"pair": f"{a}+{b}", "d1": r["d1"], "d2": r["d2"], "reg_cap": r["reg_cap"], "regs": m.info.regs,
                "blocks_per_sm": m.info.blocks_per_sm, "a_us": ta, "b_us": tb, "seq_us": t["sequential"],
                "two_stream_us": t["two_stream"], "fused_us": tf,
@@ -501,6 +530,7 @@ def crypto_suite(hf, torch, args, rank, world, stream):
         if b == "ethash":
             res["dag_bytes"] = wb.dag_bytes
             res["dag_gbs_fused"] = CRYPTO_COUNTS[b] * 64 * 128 / (tf * 1e3)
+        res["roofline"] = crypto_roofline({a: CRYPTO_COUNTS[a], b: CRYPTO_COUNTS[b]}, tf, sm_mhz, hbm_peak)
         # the single exchange: total hits + winning nonce over all ranks
         img_out = hf.Image(wa.image).merge(hf.Image(wb.image)).upload(stream)
         m.run(img_out, grid, stream)
@@ -523,8 +553,8 @@ def crypto_suite(hf, torch, args, rank, world, stream):
     su = P.source("b200", "upsample")
     ku = hf.Module.kernel(su, grid=grid, specialize=img)
     kb = hf.Module.kernel(srcs["blake256"], grid=grid, specialize=img)
-    seq = hf.time("sequential", ku, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["median_us"]
-    two = hf.time("two_stream", ku, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["median_us"]
+    seq = hf.time("sequential", ku, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
+    two = hf.time("two_stream", ku, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
     sweep = []
     for d0 in (640, 768, 896, 1024):
         try:
@@ -538,6 +568,14 @@ def crypto_suite(hf, torch, args, rank, world, stream):
     best = min(sweep, key=lambda x: x["us"])
     out["c4"] = {"pair": "upsample+blake256", "seq_us": seq, "two_stream_us": two, "best": best,
                  "speedup": min(seq, two) / best["us"], "sweep": sweep}
+    # C4 pair roofline: max(Upsample's HBM time, BLAKE-256's issue time)
+    rb = crypto_roofline({"blake256": 1 << 21}, best["us"], sm_mhz, hbm_peak)
+    if rb is not None:
+        t_hbm = wu.bytes / (hbm_peak * 1e3)
+        t_roof = max(t_hbm, rb["issue_us"])
+        out["c4"]["roofline"] = {"bound": "hbm" if t_hbm >= rb["issue_us"] else "issue", "roofline_us": t_roof,
+                                 "frac": t_roof / best["us"], "hbm_us": t_hbm, "issue_us": rb["issue_us"],
+                                 "alu_pipe_us": rb["alu_pipe_us"]}
     return out
 
 

@@ -78,9 +78,10 @@ typedef struct hf_timing {
   double mean_us;
   double max_us;
   int reps;
+  double iqm_us; /* mean of the middle half (event timestamps tick every 2.048 us) */
 } hf_timing;
 
-/* search.hpp:11-15 EvalOutcome (device backend: cycles = median ns). */
+/* search.hpp:11-15 EvalOutcome (device backend: cycles = interquartile-mean ns). */
 typedef struct hf_eval {
   long long cycles;
   double occupancy;

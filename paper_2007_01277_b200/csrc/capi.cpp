@@ -389,7 +389,7 @@ int hf_time(int mode, const hf_module* a, const hf_module* b, hf_image* img, int
                                                    : hf::rt::Mode::Single;
     hf::rt::Timing t = hf::rt::time(md, a->m, b ? &b->m : nullptr, img->img, grid_a, grid_b, warmup, reps,
                                     flush_l2 != 0, stream);
-    *out = hf_timing{t.median_us, t.min_us, t.mean_us, t.max_us, t.reps};
+    *out = hf_timing{t.median_us, t.min_us, t.mean_us, t.max_us, t.reps, t.iqm_us};
   });
 }
 
@@ -400,8 +400,8 @@ int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, h
     hf::rt::Timing t =
         hf::rt::time(hf::rt::Mode::Single, m, nullptr, img->img, grid, 0, warmup, reps, flush_l2 != 0, nullptr);
     hf::rt::Props p = hf::rt::props();
-    out->us = t.median_us;
-    out->cycles = (long long)(t.median_us * 1000.0 + 0.5);
+    out->us = t.iqm_us;
+    out->cycles = (long long)(t.iqm_us * 1000.0 + 0.5);
     out->occupancy = double(m.blocks_per_sm) * (d1 + d2) / double(p.max_threads_per_sm);
     out->utilization = 0.0;
     out->regs = m.regs;

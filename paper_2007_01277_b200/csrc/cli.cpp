@@ -255,8 +255,8 @@ int cmd_profile(const Args& a) {
   }
   rt::Module m = rt::compile(k, cap);
   rt::Timing t = rt::time(rt::Mode::Single, m, nullptr, img, a.grid, 0, a.warmup, a.reps, true);
-  std::printf("%lld\n", (long long)(t.median_us * 1000.0 + 0.5));
-  std::printf("us = %.3f\nregisters = %d\nblocks_per_sm = %d\n", t.median_us, m.regs, m.blocks_per_sm);
+  std::printf("%lld\n", (long long)(t.iqm_us * 1000.0 + 0.5));
+  std::printf("us = %.3f\nregisters = %d\nblocks_per_sm = %d\n", t.iqm_us, m.regs, m.blocks_per_sm);
   rt::unload(m);
   return 0;
 }

@@ -467,6 +467,8 @@ Timing time(Mode mode, const Module& a, const Module* b, Image& img, int grid_a,
   t.min_us = sorted.front();
   t.max_us = sorted.back();
   t.mean_us = std::accumulate(us.begin(), us.end(), 0.0) / double(us.size());
+  size_t lo = sorted.size() / 4, hi = sorted.size() - sorted.size() / 4;
+  t.iqm_us = std::accumulate(sorted.begin() + lo, sorted.begin() + hi, 0.0) / double(hi - lo);
   return t;
 }
 

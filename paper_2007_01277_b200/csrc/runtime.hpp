@@ -63,6 +63,10 @@ void launch_raw(const Module& m, int grid, void** args, void* stream = nullptr);
 struct Timing {
   double median_us = 0, min_us = 0, mean_us = 0, max_us = 0;
   int reps = 0;
+  // Interquartile mean. CUDA event timestamps on the B200 tick every 2.048 us; the start phase
+  // of each repetition is random against that tick, so the mean of the middle half resolves
+  // below one tick where the median cannot.
+  double iqm_us = 0;
 };
 enum class Mode { Single, Sequential, TwoStream };
 // Times `a` (Single) or the pair a;b (Sequential) / a||b on two streams (TwoStream).

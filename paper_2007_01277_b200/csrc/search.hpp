@@ -16,10 +16,10 @@
 namespace hf {
 
 struct EvalOutcome {
-  int64_t cycles = 0;        // device backend: nanoseconds (median)
+  int64_t cycles = 0;        // device backend: nanoseconds (interquartile mean)
   double occupancy = 0.0;
   double utilization = 0.0;
-  double us = 0.0;           // device backend: median microseconds
+  double us = 0.0;           // device backend: interquartile-mean microseconds
   int regs = 0;
 };
 

@@ -79,7 +79,7 @@ class _ModInfo(C.Structure):
 
 class _Timing(C.Structure):
     _fields_ = [("median_us", C.c_double), ("min_us", C.c_double), ("mean_us", C.c_double),
-                ("max_us", C.c_double), ("reps", C.c_int)]
+                ("max_us", C.c_double), ("reps", C.c_int), ("iqm_us", C.c_double)]
 
 
 class _Eval(C.Structure):
@@ -498,7 +498,7 @@ def time(mode: str, a: Module, b: Optional[Module], img: Image, grid_a: int = 0,
     _check(_lib.hf_time(TIME_MODES[mode], a._h, b._h if b else None, img._h, grid_a, grid_b, warmup, reps,
                         int(flush_l2), _stream(stream), C.byref(t), C.byref(err)), err)
     return {"median_us": t.median_us, "min_us": t.min_us, "mean_us": t.mean_us, "max_us": t.max_us,
-            "reps": t.reps}
+            "reps": t.reps, "iqm_us": t.iqm_us}
 
 
 def profile(src1: str, src2: str, d1: int, d2: int, img: Image, regcap="off", grid: int = 0,
