@@ -399,7 +399,9 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom["pair"])
+            # ncu dram__bytes_read.sum + dram__bytes_write.sum of this fused kernel, one launch
+            # (scripts/ncu_members.py under ncu -> scripts/ncu_summarize.py traffic)
+            traffic = json.load(open(tpath))[dom["pair"]]["dram_bytes"]
         except Exception:
             traffic = None
 
