@@ -230,7 +230,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hfuse", choices=["hfuse", "reference"])
-    ap.add_argument("--grid", type=int, default=296, help="common grid of the fused pairs (148 SMs x 2)")
+    ap.add_argument("--grid", type=int, default=296, help="crypto suite grid (148 SMs x 2 blocks)")
+    ap.add_argument("--grids", default="296,592,1184,2368",
+                    help="launch grids tried for every DL member and fused pair (multiples of 148 SMs)")
     ap.add_argument("--search-reps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pairs", default="all")
@@ -253,7 +255,7 @@ def main():
 
     pair_list = P.PAIRS if args.pairs == "all" else [tuple(p.split("+")) for p in args.pairs.split(",")]
     keys = sorted({k for p in pair_list for k in p})
-    grid = args.grid
+    grids = [int(g) for g in args.grids.split(",")] if args.grids else [args.grid]
     stream = torch.cuda.current_stream()
 
     # ---- setup: one image holding every member's arrays (bound by name), per-rank shard seed
@@ -264,37 +266,56 @@ def main():
     work = {k: P.MEMBERS[k].sizes["full"](rank) for k in keys}
     src = {k: P.source("b200", P.MEMBERS[k].stem) for k in keys}
     # JIT specialization: every module folds this image's scalar shapes into its code
-    unfused = {k: hf.Module.kernel(src[k], grid=grid, specialize=img) for k in keys}
+    unfused = {k: hf.Module.kernel(src[k], grid=grids[0], specialize=img) for k in keys}
+    # The members are grid-stride loops, so the launch grid is a free parameter. Every variant
+    # gets its own best grid: each unfused member alone (the baselines), each fused pair jointly
+    # with its split and register cap (the search is repeated per grid; the compiled candidates
+    # are cached, so only the timing repeats).
+    mgrid, member_sweep = {}, {}
+    for k in keys:
+        ts = {g: hf.time("single", unfused[k], None, img, g, warmup=2, reps=10, stream=stream)["iqm_us"]
+              for g in grids}
+        mgrid[k] = min(ts, key=ts.get)
+        member_sweep[k] = {str(g): round(t, 2) for g, t in ts.items()}
 
     results = []
     fused = {}
+    pgrid = {}
     t_setup = time.perf_counter()
     for a, b in pair_list:
-        r = hf.search(src[a], src[b], img, d0=1024, grid=grid, reps=args.search_reps, warmup=2, specialize=True)
+        r, grid, trace = None, None, []
+        for g in grids:
+            rg = hf.search(src[a], src[b], img, d0=1024, grid=g, reps=args.search_reps, warmup=2, specialize=True)
+            trace += [(g, t["d1"], t["reg_cap"], round(t["us"], 2)) for t in rg["trace"]]
+            if r is None or rg["best_time"] < r["best_time"]:
+                r, grid = rg, g
         cap = r["reg_cap"]
         m = hf.Module.fused(src[a], src[b], r["d1"], r["d2"], regcap=cap if cap else "off", grid=grid,
                             specialize=img)
         fused[(a, b)] = m
-        # one protocol for all three variants: L2 flushed (clean) before every repetition
+        pgrid[(a, b)] = grid
+        ga, gb = mgrid[a], mgrid[b]
+        # one protocol for all variants: L2 flushed (clean) before every repetition
         fz = hf.time("single", m, None, img, grid, warmup=2, reps=20, stream=stream)
-        seq = hf.time("sequential", unfused[a], unfused[b], img, grid, grid, warmup=2, reps=20, stream=stream)
-        two = hf.time("two_stream", unfused[a], unfused[b], img, grid, grid, warmup=2, reps=20, stream=stream)
-        ta = hf.time("single", unfused[a], None, img, grid, warmup=2, reps=10, stream=stream)
-        tb = hf.time("single", unfused[b], None, img, grid, warmup=2, reps=10, stream=stream)
+        seq = hf.time("sequential", unfused[a], unfused[b], img, ga, gb, warmup=2, reps=20, stream=stream)
+        two = hf.time("two_stream", unfused[a], unfused[b], img, ga, gb, warmup=2, reps=20, stream=stream)
+        ta = hf.time("single", unfused[a], None, img, ga, warmup=2, reps=10, stream=stream)
+        tb = hf.time("single", unfused[b], None, img, gb, warmup=2, reps=10, stream=stream)
         # baselines of the paper's comparison: the reference's naive goto fusion of the naive
         # member forms at the same split, and vertical fusion (VFuse) of the B200 forms
         naive = hf.Module.naive(P.source("ref", P.MEMBERS[a].stem), P.source("ref", P.MEMBERS[b].stem),
                                 r["d1"], r["d2"], grid)
         tn = hf.time("single", naive, None, img, grid, warmup=2, reps=10, stream=stream)
         vert = hf.Module.vertical(src[a], src[b], grid, specialize=img)
-        tv = hf.time("single", vert, None, img, grid, warmup=2, reps=10, stream=stream)
-        results.append({"pair": f"{a}+{b}", "d1": r["d1"], "d2": r["d2"], "reg_cap": cap,
+        tv = min(hf.time("single", vert, None, img, g, warmup=2, reps=10, stream=stream)["iqm_us"] for g in grids)
+        results.append({"pair": f"{a}+{b}", "grid": grid, "d1": r["d1"], "d2": r["d2"], "reg_cap": cap,
+                        "grid_a": ga, "grid_b": gb,
                         "bytes": work[a].bytes + work[b].bytes, "regs": m.info.regs,
                         "blocks_per_sm": m.info.blocks_per_sm, "fused_us": fz["iqm_us"],
                         "seq_us": seq["iqm_us"], "two_stream_us": two["iqm_us"],
                         "a_us": ta["iqm_us"], "b_us": tb["iqm_us"],
-                        "naive_fused_us": tn["iqm_us"], "vertical_us": tv["iqm_us"],
-                        "search_trace": [(t["d1"], t["reg_cap"], round(t["us"], 2)) for t in r["trace"]]})
+                        "naive_fused_us": tn["iqm_us"], "vertical_us": tv,
+                        "search_trace": trace})
     setup_s = time.perf_counter() - t_setup
 
     import ctypes
@@ -321,7 +342,7 @@ def main():
         for i, (a, b) in enumerate(pair_list):
             if record is not None:
                 record[i][0].record(stream)
-            fused[(a, b)].run(img, grid, stream)
+            fused[(a, b)].run(img, pgrid[(a, b)], stream)
             if record is not None:
                 record[i][1].record(stream)
         if dist is not None:
@@ -333,8 +354,8 @@ def main():
         # the same ten pairs unfused, each pair's two kernels concurrent on two streams
         for a, b in pair_list:
             side.wait_stream(stream)
-            unfused[a].run(img, grid, stream)
-            unfused[b].run(img, grid, side)
+            unfused[a].run(img, mgrid[a], stream)
+            unfused[b].run(img, mgrid[b], side)
             stream.wait_stream(side)
         if dist is not None:
             reduce_outputs()
@@ -387,7 +408,7 @@ def main():
     achieved = dom["bytes"] / (dom["in_step_us_mean"] * 1e3)  # GB/s, mean launch time inside the step
 
     # ---- e2e: the same step through the C ABI from pinned host buffers
-    e2e = e2e_step(hf, torch, P, pair_list, fused, work, keys, grid, stream, args)
+    e2e = e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args)
     del img  # free the DL images before the crypto suite (the Ethash DAG alone is 4 GiB)
     crypto_res = None
     clk = clocks.summary()
@@ -431,7 +452,8 @@ def main():
         "data": "synthetic (splitmix64-seeded in HBM; per-rank shard seed)",
         "config": {"workload": "C2: all 10 DL pairs of {BatchNorm-stats 64x256x56x56, Hist 64x256x56x56, "
                                "Im2Col 32x64x56x56, MaxPool 64x64x112x112, Upsample 64x256x28x28} fused at the "
-                               "searched best split (d0=1024)", "grid": grid, "pairs": len(results),
+                               "searched best (grid, split, register cap) at d0=1024", "grids": grids,
+                   "pairs": len(results), "member_grid_us": member_sweep,
                    "l2": "inputs per pair >= 410 MB > 126 MB L2 (no flush)", "parallelism": f"dp{world} (batch shards)"},
         "speedup_geomean": geo,
         "unfused_two_stream_step_us": unfused_us_per_step,
@@ -581,7 +603,7 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
     return out
 
 
-def e2e_step(hf, torch, P, pair_list, fused, work, keys, grid, stream, args):
+def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):
     """Host-buffer end-to-end step via hf_launch: per pair, pinned-host -> HBM copies of the
     pair's inputs, the fused launch, HBM -> pinned-host copies of its outputs."""
     host, dev = {}, {}
@@ -617,7 +639,7 @@ def e2e_step(hf, torch, P, pair_list, fused, work, keys, grid, stream, args):
                     args_[p["name"]] = dev[p["name"]]
                 else:
                     args_[p["name"]] = scal[p["name"]]
-            m.launch(args_, grid=grid, stream=stream)
+            m.launch(args_, grid=pgrid[(a, b)], stream=stream)
             for p in m.params:
                 if p["array"] and p["written"]:
                     host[p["name"]].copy_(dev[p["name"]], non_blocking=True)

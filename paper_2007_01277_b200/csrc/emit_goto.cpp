@@ -143,6 +143,10 @@ struct GotoPrinter {
         pad(ind);
         o += "__syncthreads();\n";
         break;
+      case SK::Fence:
+        pad(ind);
+        o += "__threadfence();\n";
+        break;
       case SK::BarSync:
         pad(ind);
         o += "asm(\"bar.sync " + std::to_string(s.bid) + ", " + std::to_string(s.bcount) + ";\");\n";

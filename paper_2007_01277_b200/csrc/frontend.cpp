@@ -5,7 +5,8 @@
 // language; Dialect::B200 (default) adds the MK+ extensions the B200 member kernels use:
 //   hex literals (0x..., wrapping to int32), `unroll [N] for (...)`,
 //   vload(arr, i, d0..dn-1) / vstore(arr, i, e0..en-1) with n in {2, 4},
-//   shr_u / rotr / rotl / ltu integer helpers.
+//   shr_u / rotr / rotl / ltu integer helpers, fence() (device-scope memory fence for
+//   inter-block hand-offs; reads of global arrays the kernel writes go through L2).
 // Each extension has an exact plain-MK expansion (downlower.cpp).
 #include <cctype>
 #include <cmath>
@@ -557,6 +558,14 @@ class Parser {
           }
           if ((at_ident("vload") || at_ident("vstore")) && at(T::LParen, 1))
             return vector_access(p);
+          if (at_ident("fence") && at(T::LParen, 1) && at(T::RParen, 2)) {
+            next();
+            next();
+            next();
+            want(T::Semi);
+            s.k = SK::Fence;
+            return s;
+          }
         }
         if (at(T::Colon, 1)) {
           s.k = SK::Label;

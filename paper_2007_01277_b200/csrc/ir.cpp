@@ -278,7 +278,8 @@ bool has_calls(const Block& b) {
 bool uses_extensions(const Kernel& k) {
   bool ext = false;
   walk(k.body, [&](const Stmt& s) {
-    if (s.k == SK::VLoad || s.k == SK::VStore || (s.k == SK::For && s.unroll != 0)) ext = true;
+    if (s.k == SK::VLoad || s.k == SK::VStore || s.k == SK::Fence || (s.k == SK::For && s.unroll != 0))
+      ext = true;
     exprs_of(s, [&](const Expr& e) {
       walk_expr(e, [&](const Expr& x) {
         if (x.k == EK::Intrin && intr_is_extension(Intr(x.i))) ext = true;
@@ -482,6 +483,10 @@ struct MkPrinter {
       case SK::Sync:
         pad(ind);
         o += "syncthreads();\n";
+        break;
+      case SK::Fence:
+        pad(ind);
+        o += "fence();\n";
         break;
       case SK::BarSync:
         pad(ind);

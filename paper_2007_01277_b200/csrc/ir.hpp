@@ -87,6 +87,7 @@ enum class SK : uint8_t {
   Decl, Assign, If, For, While, Sync, BarSync, Atomic, Return, Call, Label, Goto,
   VLoad,   // MK+: vload(arr, i, d0..dn-1): d_k = arr[i*n + k], index evaluated once
   VStore,  // MK+: vstore(arr, i, e0..en-1): arr[i*n + k] = e_k
+  Fence,   // MK+: fence(): device-scope memory fence (a no-op for the sequential interpreter)
 };
 
 struct Stmt {

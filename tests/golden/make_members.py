@@ -24,6 +24,7 @@ from paper_2007_01277_b200 import pairs  # noqa: E402
 
 GRID = 4
 SPLITS = [256, 512, 768]
+BN_GRIDS = [3, 7, 16, 37]
 OUTPUTS = {"bn": ["bn_stats"], "hist": ["hi_out"], "maxpool": ["mp_y", "mp_idx"], "upsample": ["us_y"],
            "im2col": ["ic_col"]}
 
@@ -68,6 +69,17 @@ def main():
                 row[str(d1)] = {"digest": dig,
                                 "outputs": {n: bits(arrays[n]) for n in OUTPUTS[a] + OUTPUTS[b]}}
             out["pairs"][f"{a}+{b}"] = row
+        # the grid-balanced BatchNorm at grids where channels straddle blocks (and, at tiny
+        # size with grid 16 > its 12 vectors, where some blocks own no vectors)
+        out["bn_grids"] = {}
+        for size in ("tiny", "parity"):
+            img = os.path.join(d, f"bn_{size}_grids.img")
+            with open(img, "w") as f:
+                f.write(pairs.MEMBERS["bn"].sizes[size](0).image)
+            out["bn_grids"][size] = {}
+            for g in BN_GRIDS:
+                dig, _, _ = oracle.ref_run("run", lowered["bn"], "--mem", img, "--grid", g)
+                out["bn_grids"][size][str(g)] = dig
     with open(os.path.join(HERE, "members.json"), "w") as f:
         json.dump(out, f, sort_keys=True)
     print("members fixtures written")
