@@ -166,7 +166,8 @@ int hf_get_device_props(hf_device_props* out, hf_error* err);
  * (JIT specialization; hf_run/hf_launch then require the same values). */
 int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regcap, int grid,
                    int min_blocks, const hf_image* specialize, hf_module** out, hf_error* err);
-/* One unfused kernel at its declared dims (regcap: HF_REGCAP_OFF or a cap). */
+/* One unfused kernel at its declared dims (regcap: HF_REGCAP_OFF = none, HF_REGCAP_AUTO = the
+ * kernel's `//@ regcap=` annotation if present (the reference's exec.cpp:954), or a cap). */
 int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks,
                     const hf_image* specialize, hf_module** out, hf_error* err);
 /* The reference's naive goto emission (fuser.cpp:290-549) of the same pair, made launchable

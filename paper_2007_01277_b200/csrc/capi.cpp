@@ -209,6 +209,7 @@ int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks, const
     o.specialize = scalars_of(specialize);
     std::optional<int> cap;
     if (regcap > 0) cap = regcap;
+    else if (regcap != HF_REGCAP_OFF && l.kernel.regcap) cap = l.kernel.regcap;  // `//@ regcap=` (exec.cpp:954)
     auto h = std::make_unique<hf_module>();
     h->m = hf::rt::compile(hf::emit_sm100(l.kernel, l.prog.funcs, o), cap);
     *out = h.release();

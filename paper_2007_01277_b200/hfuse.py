@@ -405,7 +405,8 @@ class Module:
     def kernel(cls, src: str, regcap=None, grid: int = 0, min_blocks: int = 0,
                specialize: Optional["Image"] = None) -> "Module":
         h, err = C.c_void_p(), _Err()
-        cap = -1 if regcap in (None, "off") else int(regcap)
+        # None: the kernel's own `//@ regcap=` annotation (if any); "off": no cap at all
+        cap = -1 if regcap == "off" else (0 if regcap is None else int(regcap))
         _check(_lib.hf_build_kernel(src.encode(), cap, grid, min_blocks, specialize._h if specialize else None,
                                     C.byref(h), C.byref(err)), err)
         return cls(h)

@@ -17,8 +17,9 @@
 //    bn_stats and clears bn_cnt[c] for the next launch. The merge order does not depend on
 //    which block arrives last, so the result is bit-identical to the sequential interpreter.
 //  * 128-bit coalesced loads, two in flight per thread, ~4 FP ops per element.
-// Requires HW % 4 == 0 and bn_P >= gridDim.x / C + 2.
-//@ grid=256
+// Requires HW % 4 == 0, C * N * HW / 4 >= gridDim.x and bn_P >= gridDim.x / C + 2.
+// regcap 32 keeps two 1024-thread blocks per SM (the rare merge path may spill).
+//@ grid=256 regcap=32
 kernel bn_stats(float bn_x[], float bn_stats[], int bn_pn[], float bn_pa[], float bn_pm[], int bn_cnt[],
                 int bn_N, int bn_C, int bn_HW, int bn_P) dims (1024, 1, 1) {
   shared int bn_sn[32];
@@ -54,12 +55,32 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_pn[], float bn_pa[], floa
       int b0 = (s0 + tid) / hw4;
       K = bn_x[((b0 * bn_C + c) * hw4 + s0 + tid - b0 * hw4) * 4];
     }
-    for (int j = s0 + tid; j < s1; j = j + 2 * nthr) {
-      int j2 = min(j + nthr, s1 - 1);
+    // main loop: both vectors in range, two independent 128-bit loads issued back to back
+    int j = s0 + tid;
+    while (j + nthr < s1) {
       int p1 = j / hw4;
-      int p2 = j2 / hw4;
+      int p2 = (j + nthr) / hw4;
       vload(bn_x, (p1 * bn_C + c) * hw4 + j - p1 * hw4, v0, v1, v2, v3);
-      vload(bn_x, (p2 * bn_C + c) * hw4 + j2 - p2 * hw4, v4, v5, v6, v7);
+      vload(bn_x, (p2 * bn_C + c) * hw4 + j + nthr - p2 * hw4, v4, v5, v6, v7);
+      float e0 = v0 - K;
+      float e1 = v1 - K;
+      float e2 = v2 - K;
+      float e3 = v3 - K;
+      sa = sa + ((e0 + e1) + (e2 + e3));
+      sb = sb + ((e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3));
+      e0 = v4 - K;
+      e1 = v5 - K;
+      e2 = v6 - K;
+      e3 = v7 - K;
+      sa = sa + ((e0 + e1) + (e2 + e3));
+      sb = sb + ((e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3));
+      n = n + 8;
+      j = j + 2 * nthr;
+    }
+    // tail: at most one vector left
+    if (j < s1) {
+      int p1 = j / hw4;
+      vload(bn_x, (p1 * bn_C + c) * hw4 + j - p1 * hw4, v0, v1, v2, v3);
       float e0 = v0 - K;
       float e1 = v1 - K;
       float e2 = v2 - K;
@@ -67,15 +88,6 @@ kernel bn_stats(float bn_x[], float bn_stats[], int bn_pn[], float bn_pa[], floa
       sa = sa + ((e0 + e1) + (e2 + e3));
       sb = sb + ((e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3));
       n = n + 4;
-      if (j + nthr < s1) {
-        e0 = v4 - K;
-        e1 = v5 - K;
-        e2 = v6 - K;
-        e3 = v7 - K;
-        sa = sa + ((e0 + e1) + (e2 + e3));
-        sb = sb + ((e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3));
-        n = n + 4;
-      }
     }
     fac = 1.0 / fmaxf(1.0, n);
     avg = K + sa * fac;
