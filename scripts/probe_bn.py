@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")
 from paper_2007_01277_b200 import hfuse as hf  # noqa: E402
 from paper_2007_01277_b200 import pairs as P  # noqa: E402
 
-base = P.source("b200", "batchnorm")
+base = P.source("b200", "batchnorm_balanced")
 start = base.index("        fence();\n        atomic_add")
 end = base.index("          bn_cnt[c] = 0;\n        }\n") + len("          bn_cnt[c] = 0;\n        }\n")
 variants = {
@@ -16,7 +16,7 @@ variants = {
     "fence_atomic_only": base[:start] + "        fence();\n        atomic_add(bn_cnt[c], 1);\n" + base[end:],
     "no_fence": base.replace("fence();", ""),
     "full_nocap": base.replace(" regcap=32", ""),
-    "v1_block_per_channel": open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "bn_v1.mk")).read(),
+    "block_per_channel": P.source("b200", "batchnorm"),
 }
 img = P.MEMBERS["bn"].sizes["full"](0)
 im = hf.Image(img.image).upload()

@@ -145,11 +145,11 @@ def test_naive_goto_fusion_runs(gpu):
 @pytest.mark.parametrize("grid", [3, 7, 16, 37])
 @pytest.mark.parametrize("size", ["tiny", "parity"])
 def test_grid_balanced_bn_matches_interpreter(gpu, size, grid):
-    """The grid-balanced BatchNorm (cross-block partials + arrival counters) equals the
+    """The grid-balanced BatchNorm variant (cross-block partials + arrival counters) equals the
     interpreter bit for bit at grids where channels straddle blocks or blocks own nothing;
     a second launch on the same image gives the same digest (counters were cleared)."""
     hf = gpu
-    mod = hf.Module.kernel(pairs.source("b200", "batchnorm"), grid=grid)
+    mod = hf.Module.kernel(pairs.source("b200", "batchnorm_balanced"), grid=grid)
     img = image(hf, "bn", size=size).upload()
     for _ in range(2):
         mod.run(img, grid)
@@ -160,12 +160,18 @@ def test_grid_balanced_bn_matches_interpreter(gpu, size, grid):
 @pytest.mark.gpu
 @pytest.mark.parametrize("grid", [296, 1184, 2368])
 def test_full_size_bn_any_grid(gpu, grid):
-    """Full C2 BatchNorm at the bench's grids vs fp64 statistics, three launches back to back."""
+    """Both BatchNorm forms at the bench's grids vs fp64 statistics, three launches back to back."""
     hf = gpu
     img = image(hf, "bn", size="full").upload()
-    mod = hf.Module.kernel(pairs.source("b200", "batchnorm"), grid=grid, specialize=img)
+    mod = hf.Module.kernel(pairs.source("b200", "batchnorm_balanced"), grid=grid, specialize=img)
     for _ in range(3):
         mod.run(img, grid)
     img.download()
     check_full("bn", img)
     assert int(np.abs(img.array("bn_cnt")).max()) == 0
+    mod = hf.Module.kernel(pairs.source("b200", "batchnorm"), grid=grid, specialize=img)
+    img.upload()
+    for _ in range(3):
+        mod.run(img, grid)
+    img.download()
+    check_full("bn", img)
