@@ -234,6 +234,8 @@ def main():
     ap.add_argument("--grids", default="296,592,1184,2368",
                     help="launch grids tried for every DL member and fused pair (multiples of 148 SMs)")
     ap.add_argument("--search-reps", type=int, default=5)
+    ap.add_argument("--granularity", type=int, default=64,
+                    help="split step of the partition sweep (the reference sweeps 128)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pairs", default="all")
     ap.add_argument("--no-crypto", action="store_true", help="skip the C3/C4 crypto suite")
@@ -285,7 +287,8 @@ def main():
     for a, b in pair_list:
         r, grid, trace = None, None, []
         for g in grids:
-            rg = hf.search(src[a], src[b], img, d0=1024, grid=g, reps=args.search_reps, warmup=2, specialize=True)
+            rg = hf.search(src[a], src[b], img, d0=1024, grid=g, reps=args.search_reps, warmup=2, specialize=True,
+                           granularity=args.granularity)
             trace += [(g, t["d1"], t["reg_cap"], round(t["us"], 2)) for t in rg["trace"]]
             if r is None or rg["best_time"] < r["best_time"]:
                 r, grid = rg, g

@@ -17,6 +17,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <atomic>
 #include <numeric>
 
 #include "runtime.hpp"
@@ -232,6 +234,82 @@ void cache_put(uint64_t key, const std::vector<char>& cubin) {
 }
 }  // namespace
 
+namespace {
+// Source as compiled (register cap applied), NVRTC options and the cache key.
+struct Prepared {
+  std::string source;
+  std::vector<std::string> opts;
+  uint64_t key = 0;
+};
+
+Prepared prepare(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) {
+  Prepared p;
+  p.opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-fmad=false"};
+  if (lineinfo) p.opts.push_back("-lineinfo");
+  p.source = k.source;
+  if (maxrreg) {
+    // --maxrregcount is ignored for kernels that carry __launch_bounds__, so a register cap
+    // replaces the emitted launch bounds with __maxnreg__ (the two cannot be combined).
+    size_t at = p.source.find("__launch_bounds__(");
+    if (at != std::string::npos) {
+      size_t end = p.source.find(')', at);
+      p.source.replace(at, end - at + 1, "__maxnreg__(" + std::to_string(*maxrreg) + ")");
+    } else {
+      p.opts.push_back("--maxrregcount=" + std::to_string(*maxrreg));
+    }
+  }
+  p.key = fnv(k.entry, fnv(p.source));
+  for (const auto& o : p.opts) p.key = fnv(o, p.key);
+  return p;
+}
+
+// NVRTC -> CUBIN through the cache. Throws Code::Compile with the log on failure.
+std::vector<char> cubin_of(const Sm100Kernel& k, const Prepared& p, std::string* log_out) {
+  std::vector<char> cubin;
+  if (cache_get(p.key, cubin)) return cubin;
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, p.source.c_str(), (k.entry + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    raise(Code::Compile, "nvrtcCreateProgram failed");
+  std::vector<const char*> argv;
+  for (const auto& o : p.opts) argv.push_back(o.c_str());
+  nvrtcResult r = nvrtcCompileProgram(prog, int(argv.size()), argv.data());
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string log(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, log.data());
+  if (log_out) *log_out = log;
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    raise(Code::Compile, "NVRTC failed for '" + k.entry + "': " + log);
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin.resize(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  cache_put(p.key, cubin);
+  return cubin;
+}
+}  // namespace
+
+void precompile(const std::vector<std::pair<Sm100Kernel, std::optional<int>>>& ks, bool lineinfo) {
+  unsigned hw = std::thread::hardware_concurrency();
+  size_t workers = std::min<size_t>(ks.size(), std::max(1u, std::min(hw, 16u)));
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> pool;
+  for (size_t w = 0; w < workers; ++w)
+    pool.emplace_back([&] {
+      for (size_t i = next++; i < ks.size(); i = next++) {
+        try {
+          cubin_of(ks[i].first, prepare(ks[i].first, ks[i].second, lineinfo), nullptr);
+        } catch (...) {
+          // reported by the compile() that needs this module
+        }
+      }
+    });
+  for (auto& t : pool) t.join();
+}
+
 Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) {
   Module m;
   m.entry = k.entry;
@@ -242,47 +320,9 @@ Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) 
   m.params = k.params;
   m.barriers = k.barriers;
   m.maxrreg = maxrreg;
-
-  std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-fmad=false"};
-  if (lineinfo) opts.push_back("-lineinfo");
-  std::string source = k.source;
-  if (maxrreg) {
-    // --maxrregcount is ignored for kernels that carry __launch_bounds__, so a register cap
-    // replaces the emitted launch bounds with __maxnreg__ (the two cannot be combined).
-    size_t at = source.find("__launch_bounds__(");
-    if (at != std::string::npos) {
-      size_t end = source.find(')', at);
-      source.replace(at, end - at + 1, "__maxnreg__(" + std::to_string(*maxrreg) + ")");
-    } else {
-      opts.push_back("--maxrregcount=" + std::to_string(*maxrreg));
-    }
-  }
-  m.source = source;
-  uint64_t key = fnv(k.entry, fnv(source));
-  for (const auto& o : opts) key = fnv(o, key);
-  if (!cache_get(key, m.cubin)) {
-    nvrtcProgram prog;
-    if (nvrtcCreateProgram(&prog, source.c_str(), (k.entry + ".cu").c_str(), 0, nullptr, nullptr) !=
-        NVRTC_SUCCESS)
-      raise(Code::Compile, "nvrtcCreateProgram failed");
-    std::vector<const char*> argv;
-    for (const auto& o : opts) argv.push_back(o.c_str());
-    nvrtcResult r = nvrtcCompileProgram(prog, int(argv.size()), argv.data());
-    size_t log_size = 0;
-    nvrtcGetProgramLogSize(prog, &log_size);
-    m.log.resize(log_size);
-    if (log_size) nvrtcGetProgramLog(prog, m.log.data());
-    if (r != NVRTC_SUCCESS) {
-      nvrtcDestroyProgram(&prog);
-      raise(Code::Compile, "NVRTC failed for '" + k.entry + "': " + m.log);
-    }
-    size_t n = 0;
-    nvrtcGetCUBINSize(prog, &n);
-    m.cubin.resize(n);
-    nvrtcGetCUBIN(prog, m.cubin.data());
-    nvrtcDestroyProgram(&prog);
-    cache_put(key, m.cubin);
-  }
+  Prepared p = prepare(k, maxrreg, lineinfo);
+  m.source = p.source;
+  m.cubin = cubin_of(k, p, &m.log);
 
   if (!device_available()) return m;  // CPU hosts: compile-only (ptxas still ran)
   Driver& d = drv();

@@ -49,6 +49,10 @@ SM sm_from_device(int device = -1);
 bool device_available();
 
 Module compile(const Sm100Kernel& k, std::optional<int> maxrreg = std::nullopt, bool lineinfo = true);
+// NVRTC-compiles a batch into the CUBIN cache on a pool of host threads (no device work);
+// a later compile() of the same (kernel, cap) only loads the module. Errors are deferred
+// to that compile().
+void precompile(const std::vector<std::pair<Sm100Kernel, std::optional<int>>>& ks, bool lineinfo = true);
 void unload(Module& m);
 
 void upload(Image& img, void* stream = nullptr);

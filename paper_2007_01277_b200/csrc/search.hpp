@@ -30,6 +30,9 @@ class ProfilerBackend {
   // Per-thread resources of one constituent run alone with `threads` threads; the
   // default is the reference's estimate (machine.cpp:215-230).
   virtual Resources resources(const Kernel& k, int threads) { return resources_of(k, threads); }
+  // Called once with every candidate of a sweep before the first evaluate(); a backend may
+  // do per-candidate work ahead of time (DeviceBackend: parallel NVRTC compilation).
+  virtual void prepare(const std::vector<std::pair<Fused, FusionConfig>>& candidates) { (void)candidates; }
 };
 
 // Spawns `command <source-file>` and reads the first integer of its stdout (search.cpp:32-62).
@@ -51,6 +54,7 @@ class DeviceBackend : public ProfilerBackend {
                 bool measured_registers = true);
   EvalOutcome evaluate(const Fused& fused, const FusionConfig& cfg) override;
   Resources resources(const Kernel& k, int threads) override;
+  void prepare(const std::vector<std::pair<Fused, FusionConfig>>& candidates) override;
   void set_specialization(std::map<std::string, ScalarVal> s) { spec_ = std::move(s); }
 
  private:
