@@ -138,6 +138,24 @@ void flush_l2(cudaStream_t s) {
   HF_CUDA(cudaGetLastError());
 }
 
+// Event timestamps advance in 2.048 us ticks on the B200. After the fixed-length flush every
+// repetition would start at the same phase of that tick and its measured length would be the
+// same multiple of it; a spin of a pseudo-random 0..4095 SM cycles (~0-2 us) before the timed
+// region randomizes the phase so the mean over repetitions resolves below one tick.
+__global__ void phase_spin(long long cycles) {
+  long long t0 = clock64();
+  while (clock64() - t0 < cycles) {
+  }
+}
+
+unsigned g_phase = 0x9E3779B9u;
+
+void randomize_phase(cudaStream_t s) {
+  g_phase = g_phase * 1664525u + 1013904223u;
+  phase_spin<<<1, 32, 0, s>>>((long long)(g_phase >> 20));
+  HF_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
 bool device_available() {
@@ -488,6 +506,7 @@ Timing time(Mode mode, const Module& a, const Module* b, Image& img, int grid_a,
   std::vector<double> us;
   for (int i = 0; i < reps; ++i) {
     if (flush) flush_l2(s);
+    randomize_phase(s);
     run_once();
     HF_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
