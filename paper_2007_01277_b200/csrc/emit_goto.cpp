@@ -147,6 +147,10 @@ struct GotoPrinter {
         pad(ind);
         o += "__threadfence();\n";
         break;
+      case SK::WarpSync:
+        pad(ind);
+        o += "__syncwarp();\n";
+        break;
       case SK::BarSync:
         pad(ind);
         o += "asm(\"bar.sync " + std::to_string(s.bid) + ", " + std::to_string(s.bcount) + ";\");\n";

@@ -6,7 +6,8 @@
 //   hex literals (0x..., wrapping to int32), `unroll [N] for (...)`,
 //   vload(arr, i, d0..dn-1) / vstore(arr, i, e0..en-1) with n in {2, 4},
 //   shr_u / rotr / rotl / ltu integer helpers, fence() (device-scope memory fence for
-//   inter-block hand-offs; reads of global arrays the kernel writes go through L2).
+//   inter-block hand-offs; reads of global arrays the kernel writes go through L2),
+//   warp_sync() (__syncwarp for intra-warp shared-memory exchanges; warp-uniform use only).
 // Each extension has an exact plain-MK expansion (downlower.cpp).
 #include <cctype>
 #include <cmath>
@@ -558,12 +559,11 @@ class Parser {
           }
           if ((at_ident("vload") || at_ident("vstore")) && at(T::LParen, 1))
             return vector_access(p);
-          if (at_ident("fence") && at(T::LParen, 1) && at(T::RParen, 2)) {
-            next();
+          if ((at_ident("fence") || at_ident("warp_sync")) && at(T::LParen, 1) && at(T::RParen, 2)) {
+            s.k = next().text == "fence" ? SK::Fence : SK::WarpSync;
             next();
             next();
             want(T::Semi);
-            s.k = SK::Fence;
             return s;
           }
         }

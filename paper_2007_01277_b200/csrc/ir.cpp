@@ -278,7 +278,8 @@ bool has_calls(const Block& b) {
 bool uses_extensions(const Kernel& k) {
   bool ext = false;
   walk(k.body, [&](const Stmt& s) {
-    if (s.k == SK::VLoad || s.k == SK::VStore || s.k == SK::Fence || (s.k == SK::For && s.unroll != 0))
+    if (s.k == SK::VLoad || s.k == SK::VStore || s.k == SK::Fence || s.k == SK::WarpSync ||
+        (s.k == SK::For && s.unroll != 0))
       ext = true;
     exprs_of(s, [&](const Expr& e) {
       walk_expr(e, [&](const Expr& x) {
@@ -487,6 +488,10 @@ struct MkPrinter {
       case SK::Fence:
         pad(ind);
         o += "fence();\n";
+        break;
+      case SK::WarpSync:
+        pad(ind);
+        o += "warp_sync();\n";
         break;
       case SK::BarSync:
         pad(ind);

@@ -88,6 +88,7 @@ enum class SK : uint8_t {
   VLoad,   // MK+: vload(arr, i, d0..dn-1): d_k = arr[i*n + k], index evaluated once
   VStore,  // MK+: vstore(arr, i, e0..en-1): arr[i*n + k] = e_k
   Fence,   // MK+: fence(): device-scope memory fence (a no-op for the sequential interpreter)
+  WarpSync,  // MK+: warp_sync(): __syncwarp() (a no-op for the lock-step interpreter)
 };
 
 struct Stmt {

@@ -705,7 +705,8 @@ struct Lowerer {
     }
     c.body = block(c.body);
     c.alt = block(c.alt);
-    if (c.k == SK::Fence) return;  // the interpreter is sequentially consistent
+    if (c.k == SK::Fence) return;     // the interpreter is sequentially consistent
+    if (c.k == SK::WarpSync) return;  // ... and runs each warp in lock step
     if (c.k == SK::VLoad || c.k == SK::VStore) {
       int id = counter++;
       int n = int(c.k == SK::VLoad ? c.outs.size() : c.val.size());
