@@ -161,6 +161,7 @@ class Checker {
       case EK::Intrin: {
         switch (Intr(e.i)) {
           case Intr::CastInt: type(e.a[0]); return Ty::Int;
+          case Intr::IntRz: type(e.a[0]); return Ty::Int;
           case Intr::CastFloat: type(e.a[0]); return Ty::Float;
           case Intr::Fmaxf:
             type(e.a[0]);

@@ -73,7 +73,8 @@ struct GotoPrinter {
       case EK::Index: return e.s + "[" + ex(e.a[0]) + "]";
       case EK::Intrin:
         switch (Intr(e.i)) {
-          case Intr::CastInt: return "(int)(" + ex(e.a[0]) + ")";
+          case Intr::CastInt:
+          case Intr::IntRz: return "(int)(" + ex(e.a[0]) + ")";
           case Intr::CastFloat: return "(float)(" + ex(e.a[0]) + ")";
           default: {
             std::string t = std::string(intr_name(Intr(e.i))) + "(";

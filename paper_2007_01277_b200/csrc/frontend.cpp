@@ -7,7 +7,8 @@
 //   vload(arr, i, d0..dn-1) / vstore(arr, i, e0..en-1) with n in {2, 4},
 //   shr_u / rotr / rotl / ltu integer helpers, fence() (device-scope memory fence for
 //   inter-block hand-offs; reads of global arrays the kernel writes go through L2),
-//   warp_sync() (__syncwarp for intra-warp shared-memory exchanges; warp-uniform use only).
+//   warp_sync() (__syncwarp for intra-warp shared-memory exchanges; warp-uniform use only),
+//   int_rz(x) (int(x) where the program guarantees |x| < 2^31: a single cvt.rzi.s32).
 // Each extension has an exact plain-MK expansion (downlower.cpp).
 #include <cctype>
 #include <cmath>
@@ -826,11 +827,13 @@ class Parser {
           else if (b200() && n.text == "ltu") w = Intr::LtU;
           else if (b200() && n.text == "fshr") w = Intr::Fshr;
           else if (b200() && n.text == "fshl") w = Intr::Fshl;
+          else if (b200() && n.text == "int_rz") w = Intr::IntRz;
           if (w) {
             std::vector<Expr> a = args();
             if (int(a.size()) != intr_arity(*w))
               raise(Code::Syntax, n.text + " takes exactly " +
-                                      std::string(intr_arity(*w) == 3 ? "three" : "two") + " arguments", p);
+                                      std::string(intr_arity(*w) == 3 ? "three" : intr_arity(*w) == 1 ? "one" : "two") +
+                                      " argument(s)", p);
             e = intrin(*w, std::move(a));
             e.pos = p;
             return e;

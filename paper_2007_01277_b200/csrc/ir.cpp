@@ -38,12 +38,13 @@ const char* intr_name(Intr i) {
     case Intr::LtU: return "ltu";
     case Intr::Fshr: return "fshr";
     case Intr::Fshl: return "fshl";
+    case Intr::IntRz: return "int_rz";
   }
   return "?";
 }
 
 int intr_arity(Intr i) {
-  if (i == Intr::CastInt || i == Intr::CastFloat) return 1;
+  if (i == Intr::CastInt || i == Intr::CastFloat || i == Intr::IntRz) return 1;
   if (i == Intr::Fshr || i == Intr::Fshl) return 3;
   return 2;
 }

@@ -67,6 +67,7 @@ enum class Intr : uint8_t {
   LtU,    // unsigned less-than (0/1)
   Fshr,   // fshr(lo, hi, n): low word of (hi:lo) >> (n & 31)   (64-bit rotates in 32-bit halves)
   Fshl,   // fshl(lo, hi, n): high word of (hi:lo) << (n & 31)
+  IntRz,  // int_rz(x): int(x) for |x| < 2^31 (device: one cvt.rzi.s32); outside that range undefined
 };
 const char* intr_name(Intr i);
 int intr_arity(Intr i);

@@ -644,6 +644,7 @@ struct Lowerer {
     const Expr& x = c.a[0];
     const Expr& n = c.a.size() > 1 ? c.a[1] : c.a[0];
     switch (Intr(c.i)) {
+      case Intr::IntRz: return intrin(Intr::CastInt, {x});
       case Intr::ShrU: return shr_u(x, n);
       case Intr::Rotr: {
         Expr left = binary(Bin::Shl, x, binary(Bin::Sub, lit(32), binary(Bin::And, n, lit(31))));

@@ -1,7 +1,9 @@
 // Histogram (torch.histc analogue, PAPER.md:405-430), B200 form (MK+).
 // 64 bins over [-4, 4]: bin = int((v - lo) * nbins / (hi - lo)), v == hi -> last bin,
 // values outside [lo, hi] are ignored. Because nbins / (hi - lo) = 8 is a power of two,
-// int((v + 4) * 8) is bit-identical to the division form (both scalings are exact).
+// int((v + 4) * 8) is bit-identical to the division form (both scalings are exact); inside the
+// range guard (v + 4) * 8 is in [0, 64], so the conversion is int_rz (one cvt.rzi.s32 instead
+// of the general int() lowering, which goes through int64 for |x| >= 2^31).
 // B200 mechanics: four 128-bit coalesced loads in flight per thread per iteration
 // (n % 4 == 0; tail loads clamped in bounds and masked), warp-private shared-memory bins
 // (32 x 64 counters: contention only inside a warp), one global atomic per bin per block.
@@ -25,57 +27,57 @@ kernel hist(float hi_x[], int hi_out[], int hi_n) dims (1024, 1, 1) {
     vload(hi_x, min(j2, last), v8, v9, v10, v11);
     vload(hi_x, min(j3, last), v12, v13, v14, v15);
     if (v0 >= -4.0 && v0 <= 4.0) {
-      atomic_add(hi_bins[wb + min(int((v0 + 4.0) * 8.0), 63)], 1);
+      atomic_add(hi_bins[wb + min(int_rz((v0 + 4.0) * 8.0), 63)], 1);
     }
     if (v1 >= -4.0 && v1 <= 4.0) {
-      atomic_add(hi_bins[wb + min(int((v1 + 4.0) * 8.0), 63)], 1);
+      atomic_add(hi_bins[wb + min(int_rz((v1 + 4.0) * 8.0), 63)], 1);
     }
     if (v2 >= -4.0 && v2 <= 4.0) {
-      atomic_add(hi_bins[wb + min(int((v2 + 4.0) * 8.0), 63)], 1);
+      atomic_add(hi_bins[wb + min(int_rz((v2 + 4.0) * 8.0), 63)], 1);
     }
     if (v3 >= -4.0 && v3 <= 4.0) {
-      atomic_add(hi_bins[wb + min(int((v3 + 4.0) * 8.0), 63)], 1);
+      atomic_add(hi_bins[wb + min(int_rz((v3 + 4.0) * 8.0), 63)], 1);
     }
     if (j1 < n4) {
       if (v4 >= -4.0 && v4 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v4 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v4 + 4.0) * 8.0), 63)], 1);
       }
       if (v5 >= -4.0 && v5 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v5 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v5 + 4.0) * 8.0), 63)], 1);
       }
       if (v6 >= -4.0 && v6 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v6 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v6 + 4.0) * 8.0), 63)], 1);
       }
       if (v7 >= -4.0 && v7 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v7 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v7 + 4.0) * 8.0), 63)], 1);
       }
     }
     if (j2 < n4) {
       if (v8 >= -4.0 && v8 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v8 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v8 + 4.0) * 8.0), 63)], 1);
       }
       if (v9 >= -4.0 && v9 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v9 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v9 + 4.0) * 8.0), 63)], 1);
       }
       if (v10 >= -4.0 && v10 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v10 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v10 + 4.0) * 8.0), 63)], 1);
       }
       if (v11 >= -4.0 && v11 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v11 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v11 + 4.0) * 8.0), 63)], 1);
       }
     }
     if (j3 < n4) {
       if (v12 >= -4.0 && v12 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v12 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v12 + 4.0) * 8.0), 63)], 1);
       }
       if (v13 >= -4.0 && v13 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v13 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v13 + 4.0) * 8.0), 63)], 1);
       }
       if (v14 >= -4.0 && v14 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v14 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v14 + 4.0) * 8.0), 63)], 1);
       }
       if (v15 >= -4.0 && v15 <= 4.0) {
-        atomic_add(hi_bins[wb + min(int((v15 + 4.0) * 8.0), 63)], 1);
+        atomic_add(hi_bins[wb + min(int_rz((v15 + 4.0) * 8.0), 63)], 1);
       }
     }
   }
