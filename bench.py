@@ -529,25 +529,32 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
         kb = hf.Module.kernel(srcs[b], grid=grid, specialize=img)
         # fixed + fixed: one partition (fixed_partition_fuse); fixed + tunable (Blake256 +
         # Ethash): the tunable side gets d0 - 512 for each d0 tried
+        # every point also tries per-interval register budgets (setmaxnreg): the fused kernel
+        # no longer forces one register count on a 32-register hash and a 128-register Ethash
         best_r, traces = None, []
-        for d0 in ((1024,) if b != "ethash" else (768, 1024)):
+        for d0 in ((1024,) if b != "ethash" else (768, 896, 1024)):
             try:
                 r = hf.search(srcs[a], srcs[b], img, d0=d0, grid=grid, reps=5, warmup=2, specialize=True,
-                              extra_caps=(64, 96, 128) if b == "ethash" else ())
+                              extra_caps=(64, 96, 128) if b == "ethash" else (), interval_regs=True)
             except hf.HFuseError:
                 continue
             traces += [(x["d1"], x["d2"], x["reg_cap"], round(x["us"], 1)) for x in r["trace"]]
             if best_r is None or r["best_time"] < best_r["best_time"]:
                 best_r = r
         r = best_r
-        m = hf.Module.fused(srcs[a], srcs[b], r["d1"], r["d2"], regcap=r["reg_cap"] or "off", grid=grid,
-                            specialize=img)
+        if r["interval_regs"]:
+            m = hf.Module.fused_regs(srcs[a], srcs[b], r["d1"], r["d2"], *r["interval_regs"], grid=grid,
+                                     specialize=img)
+        else:
+            m = hf.Module.fused(srcs[a], srcs[b], r["d1"], r["d2"], regcap=r["reg_cap"] or "off", grid=grid,
+                                specialize=img)
         t = {mode: hf.time(mode, ka, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
              for mode in ("sequential", "two_stream")}
         tf = hf.time("single", m, None, img, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
         ta = hf.time("single", ka, None, img, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
         tb = hf.time("single", kb, None, img, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
-        res = {"pair": f"{a}+{b}", "d1": r["d1"], "d2": r["d2"], "reg_cap": r["reg_cap"], "regs": m.info.regs,
+        res = {"pair": f"{a}+{b}", "d1": r["d1"], "d2": r["d2"], "reg_cap": r["reg_cap"],
+               "interval_regs": r["interval_regs"], "regs": m.info.regs,
                "blocks_per_sm": m.info.blocks_per_sm, "a_us": ta, "b_us": tb, "seq_us": t["sequential"],
                "two_stream_us": t["two_stream"], "fused_us": tf,
                "speedup": min(t["sequential"], t["two_stream"]) / tf,
@@ -586,7 +593,7 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
     for d0 in (640, 768, 896, 1024):
         try:
             r = hf.search(su, srcs["blake256"], img, d0=d0, grid=grid, reps=5, warmup=2, specialize=True,
-                          extra_caps=(32, 40, 48, 64, 96))
+                          extra_caps=(32, 40, 48, 64, 96), interval_regs=True)
         except hf.HFuseError:
             continue
         for row in r["trace"]:

@@ -70,6 +70,8 @@ typedef struct hf_module_info {
   int blocks_per_sm;
   int n_params;
   int n_barriers;
+  int launch_regs;      /* per-interval budgets (hf_build_fused_regs): pool regs/thread, else 0 */
+  int interval_regs[2]; /* setmaxnreg budget of interval 1 / 2, else 0 */
 } hf_module_info;
 
 typedef struct hf_timing {
@@ -104,6 +106,10 @@ typedef struct hf_search_opts {
   int n_extra_caps;
   const int* extra_caps;    /* additional register caps per partition (C4 sweep) */
   int out_style;            /* style of *best_src */
+  int interval_regs;        /* B200: also sweep per-interval register budgets (setmaxnreg) */
+  int budget_points;        /* budget shares per partition (0: 5) */
+  int best_regs1;           /* out: budgets of the best point (0 when it has none) */
+  int best_regs2;           /* out */
 } hf_search_opts;
 
 typedef struct hf_device_props {
@@ -166,6 +172,15 @@ int hf_get_device_props(hf_device_props* out, hf_error* err);
  * (JIT specialization; hf_run/hf_launch then require the same values). */
 int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regcap, int grid,
                    int min_blocks, const hf_image* specialize, hf_module** out, hf_error* err);
+/* hf_build_fused with per-interval register budgets instead of one whole-kernel cap: the
+ * reference bounds both constituents by a single r0 (machine.cpp:269-283);
+ * on sm_100a the fused kernel is compiled with __maxnreg__(L), L*d0 >= regs1*d1 + regs2*d2,
+ * and each interval re-sizes its warpgroups with setmaxnreg.dec/.inc on entry. Requires
+ * d1, d2 multiples of 128 and budgets that are multiples of 8 in [24, 256]
+ * (HF_E_INVALID_ARGUMENT), a pool that fits one SM (HF_E_DOES_NOT_FIT), and ptxas to allocate
+ * exactly L registers (HF_E_DEVICE otherwise: an undersized pool would block the .inc). */
+int hf_build_fused_regs(const char* src1, const char* src2, int d1, int d2, int regs1, int regs2,
+                        int grid, const hf_image* specialize, hf_module** out, hf_error* err);
 /* One unfused kernel at its declared dims (regcap: HF_REGCAP_OFF = none, HF_REGCAP_AUTO = the
  * kernel's `//@ regcap=` annotation if present (the reference's exec.cpp:954), or a cap). */
 int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks,
@@ -226,7 +241,7 @@ int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, h
 
 /* search_config / fixed_partition_fuse + trace_csv (search.hpp:66-77). img may be NULL for
  * the command backend. */
-int hf_search(const char* src1, const char* src2, hf_image* img, const hf_search_opts* opts,
+int hf_search(const char* src1, const char* src2, hf_image* img, hf_search_opts* opts,
               int* best_d1, int* best_d2, int* best_regcap, long long* best_time,
               char** trace_csv, char** best_src, hf_error* err);
 

@@ -77,11 +77,24 @@ std::map<std::string, hf::ScalarVal> scalars_of(const hf_image* img) {
   return m;
 }
 
+// sm_100a fused module with per-interval register budgets (setmaxnreg).
+hf::rt::Module build_fused_regs(const char* s1, const char* s2, int d1, int d2, int regs1, int regs2, int grid,
+                                const hf_image* spec) {
+  hf::SM sm = hf::rt::device_available() ? hf::rt::sm_from_device() : hf::SM::b200();
+  hf::FuseResult r = hf::fuse_sources(s1, s2, d1, d2, "off", sm, grid);
+  if (grid > 0) r.fused.grid = grid;
+  hf::Sm100Options o;
+  o.regs1 = regs1;
+  o.regs2 = regs2;
+  o.specialize = scalars_of(spec);
+  return hf::rt::compile(hf::emit_sm100(r.fused, o), std::nullopt);
+}
+
 // sm_100a fused module; regcap AUTO means the register bound r0 with the B200 machine model.
 hf::rt::Module build_fused(const char* s1, const char* s2, int d1, int d2, int regcap, int grid, int min_blocks,
                            const hf_image* spec) {
   hf::SM sm = hf::rt::device_available() ? hf::rt::sm_from_device() : hf::SM::b200();
-  hf::FuseResult r = hf::fuse_sources(s1, s2, d1, d2, regcap_spec(regcap), sm);
+  hf::FuseResult r = hf::fuse_sources(s1, s2, d1, d2, regcap_spec(regcap), sm, grid);
   if (grid > 0) r.fused.grid = grid;
   hf::Sm100Options o;
   o.min_blocks = min_blocks;
@@ -199,6 +212,15 @@ int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regca
   });
 }
 
+int hf_build_fused_regs(const char* src1, const char* src2, int d1, int d2, int regs1, int regs2, int grid,
+                        const hf_image* specialize, hf_module** out, hf_error* err) {
+  return guarded(err, [&] {
+    auto h = std::make_unique<hf_module>();
+    h->m = build_fused_regs(src1, src2, d1, d2, regs1, regs2, grid, specialize);
+    *out = h.release();
+  });
+}
+
 int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks, const hf_image* specialize,
                     hf_module** out, hf_error* err) {
   return guarded(err, [&] {
@@ -243,7 +265,8 @@ int hf_build_vertical(const char* src1, const char* src2, int grid, const hf_ima
 int hf_module_get_info(const hf_module* m, hf_module_info* out) {
   if (!m || !out) return to_abi(hf::Code::InvalidArgument);
   *out = hf_module_info{m->m.threads, m->m.grid, m->m.smem, m->m.regs, m->m.local_bytes, m->m.blocks_per_sm,
-                        int(m->m.params.size()), int(m->m.barriers.size())};
+                        int(m->m.params.size()), int(m->m.barriers.size()), m->m.launch_regs,
+                        {m->m.interval_regs[0], m->m.interval_regs[1]}};
   return HF_OK;
 }
 
@@ -410,7 +433,7 @@ int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, h
   });
 }
 
-int hf_search(const char* src1, const char* src2, hf_image* img, const hf_search_opts* opts, int* best_d1,
+int hf_search(const char* src1, const char* src2, hf_image* img, hf_search_opts* opts, int* best_d1,
               int* best_d2, int* best_regcap, long long* best_time, char** trace, char** best_src, hf_error* err) {
   return guarded(err, [&] {
     hf_search_opts o{};
@@ -435,12 +458,18 @@ int hf_search(const char* src1, const char* src2, hf_image* img, const hf_search
     hf::SearchOptions so;
     so.granularity = o.granularity > 0 ? o.granularity : 128;
     for (int i = 0; i < o.n_extra_caps; ++i) so.extra_caps.push_back(o.extra_caps[i]);
+    so.interval_regs = o.interval_regs != 0;
+    if (o.budget_points > 0) so.budget_points = o.budget_points;
     hf::SearchResult r = (n1.tunable && n2.tunable) ? hf::search_config(n1, n2, o.d0, *be, sm, so)
                                                     : hf::fixed_partition_fuse(n1, n2, *be, sm, o.d0, so);
     if (best_d1) *best_d1 = r.best_cfg.d1;
     if (best_d2) *best_d2 = r.best_cfg.d2;
     if (best_regcap) *best_regcap = r.best_cfg.reg_cap ? *r.best_cfg.reg_cap : HF_REGCAP_OFF;
     if (best_time) *best_time = r.best_time;
+    if (opts) {
+      opts->best_regs1 = r.best_cfg.regs1;
+      opts->best_regs2 = r.best_cfg.regs2;
+    }
     if (trace) *trace = dup(hf::trace_csv(r));
     if (best_src) *best_src = dup(hf::emit(r.best, style_of(o.out_style)));
   });

@@ -1,10 +1,12 @@
 // hfuse — the B200 drop-in for the reference CLI (/root/reference/proj/tools/mkfuse.cpp).
 //
 //   hfuse fuse K1 K2 --d1 N --d2 N [--style goto|structured|sm100] [--regcap n|auto|off] [-o F] [--sm S]
+//              [--interval-regs R1,R2]   (sm100: per-interval setmaxnreg budgets instead of --regcap)
 //   hfuse simulate K [--mem IMG]... [--seed S] [--regcap n|auto|off] [--dump-mem F] [--entry E]
 //   hfuse simulate --sequential K1 K2 --mem IMG... [--dump-mem F]
 //   hfuse search K1 K2 [--d0 N] --mem IMG... [--trace F] [-o F] [--style S] [--profiler-cmd CMD]
-//                      [--granularity G] [--caps 32,40,...] [--reps N]
+//                      [--granularity G] [--caps 32,40,...] [--reps N] [--budgets]
+//                      (--budgets: also sweep per-interval setmaxnreg register budgets)
 //   hfuse occupancy [K] [--regs N --shmem B --threads T] [--sm S]
 //   hfuse check K              hfuse lower K [-o F]           hfuse emit K [-o F]
 //   hfuse profile CANDIDATE(.cu|.mk) --mem IMG... [--grid G]   (mkfuse --profiler-cmd target)
@@ -32,8 +34,8 @@ struct Args {
   std::string cmd;
   std::vector<std::string> inputs, mem;
   std::optional<uint64_t> seed;
-  std::string sm = "pascal-like", regcap = "auto", style, out, trace, entry, profiler_cmd, dump, caps;
-  bool sequential = false, sm_given = false, regcap_given = false;
+  std::string sm = "pascal-like", regcap = "auto", style, out, trace, entry, profiler_cmd, dump, caps, iregs;
+  bool sequential = false, sm_given = false, regcap_given = false, budgets = false;
   int d0 = 1024, d1 = 0, d2 = 0, regs = 0, threads = 0, granularity = 128, reps = 10, warmup = 3, grid = 0;
   int64_t shmem = 0;
 };
@@ -80,11 +82,13 @@ Args parse_args(int argc, char** argv) {
     else if (s == "--entry") a.entry = val();
     else if (s == "--dump-mem") a.dump = val();
     else if (s == "--sequential") a.sequential = true;
+    else if (s == "--budgets") a.budgets = true;
     else if (s == "--regs") a.regs = num();
     else if (s == "--shmem") a.shmem = std::stoll(val());
     else if (s == "--threads") a.threads = num();
     else if (s == "--granularity") a.granularity = num();
     else if (s == "--caps") a.caps = val();
+    else if (s == "--interval-regs") a.iregs = val();
     else if (s == "--reps") a.reps = num();
     else if (s == "--warmup") a.warmup = num();
     else if (s == "--grid") a.grid = num();
@@ -117,6 +121,24 @@ int cmd_fuse(const Args& a) {
   std::string style = a.style.empty() ? "goto" : a.style;
   Style st = style == "structured" ? Style::Structured : style == "sm100" ? Style::Sm100 : Style::Goto;
   std::string path = a.out.empty() ? (st == Style::Structured ? "fused.mk" : "fused.cu") : a.out;
+  if (!a.iregs.empty()) {
+    if (st != Style::Sm100) raise(Code::InvalidArgument, "--interval-regs needs --style sm100");
+    if (a.regcap_given && a.regcap != "off") raise(Code::InvalidArgument, "--interval-regs and --regcap are exclusive");
+    int r1 = 0, r2 = 0;
+    if (std::sscanf(a.iregs.c_str(), "%d,%d", &r1, &r2) != 2)
+      raise(Code::InvalidArgument, "--interval-regs needs R1,R2, got '" + a.iregs + "'");
+    r.fused.cfg.reg_cap.reset();
+    Sm100Options o;
+    o.regs1 = r1;
+    o.regs2 = r2;
+    Sm100Kernel k = emit_sm100(r.fused, o);
+    write_text(path, k.source);
+    r.fused.cfg.reg_cap = k.launch_regs;  // the report's occupancy: the pool per thread
+    std::fputs(fuse_report(r).c_str(), stdout);
+    std::printf("interval_regs = %d,%d (launch %d)\n", r1, r2, k.launch_regs);
+    std::printf("wrote %s\n", path.c_str());
+    return 0;
+  }
   write_text(path, emit(r.fused, st));
   std::fputs(fuse_report(r).c_str(), stdout);
   std::printf("wrote %s\n", path.c_str());
@@ -177,6 +199,7 @@ int cmd_search(const Args& a) {
   if (a.grid > 0) n1.grid = n2.grid = a.grid;
   SearchOptions so;
   so.granularity = a.granularity;
+  so.interval_regs = a.budgets;
   if (!a.caps.empty()) {
     std::stringstream ss(a.caps);
     std::string c;
@@ -186,7 +209,8 @@ int cmd_search(const Args& a) {
   Image img;
   SM sm = a.sm_given ? SM::preset_or_file(a.sm) : SM::b200();
   if (!a.profiler_cmd.empty()) {
-    be = std::make_unique<ExternalCommandBackend>(a.profiler_cmd);
+    // budgets exist only in sm100 text, so a budget sweep hands the command sm100 candidates
+    be = std::make_unique<ExternalCommandBackend>(a.profiler_cmd, a.budgets ? Style::Sm100 : Style::Goto);
   } else {
     if (!rt::device_available()) raise(Code::Device, "search times candidates on the GPU; no CUDA device is visible");
     if (!a.sm_given) sm = rt::sm_from_device();
@@ -204,6 +228,7 @@ int cmd_search(const Args& a) {
   std::printf("best_d1 = %d\n", r.best_cfg.d1);
   std::printf("best_d2 = %d\n", r.best_cfg.d2);
   std::printf("best_reg_cap = %s\n", r.best_cfg.reg_cap ? std::to_string(*r.best_cfg.reg_cap).c_str() : "none");
+  if (r.best_cfg.regs1 > 0) std::printf("best_interval_regs = %d/%d\n", r.best_cfg.regs1, r.best_cfg.regs2);
   std::printf("best_cycles = %lld\n", (long long)r.best_time);
   if (!a.trace.empty()) {
     write_text(a.trace, trace_csv(r));

@@ -30,12 +30,13 @@ Loaded load_source(const std::string& src, const std::string& entry, Dialect dia
 }
 
 FuseResult fuse_sources(const std::string& src1, const std::string& src2, int d1, int d2,
-                        const std::string& regcap, const SM& sm) {
+                        const std::string& regcap, const SM& sm, int grid) {
   FuseResult r;
   r.sm = sm;
   Loaded k1 = load_source(src1), k2 = load_source(src2);
   r.n1 = normalize(k1.kernel, k1.prog.funcs, "k1_");
   r.n2 = normalize(k2.kernel, k2.prog.funcs, "k2_");
+  if (grid > 0) r.n1.grid = r.n2.grid = grid;  // members are grid-stride: any common grid works
   r.fused = fuse(r.n1, r.n2, d1, d2, sm);
   r.r1 = resources_of(r.n1, d1);
   r.r2 = resources_of(r.n2, d2);

@@ -26,7 +26,7 @@ struct FuseResult {
 
 // regcap: "auto" (record r0), "off", or a positive integer (mkfuse.cpp:118-133).
 FuseResult fuse_sources(const std::string& src1, const std::string& src2, int d1, int d2,
-                        const std::string& regcap, const SM& sm);
+                        const std::string& regcap, const SM& sm, int grid = 0);  // grid > 0: the common launch grid (overrides both //@ grid)
 std::string fuse_report(const FuseResult& r);
 std::string emit(const Fused& f, Style style);
 std::string read_text(const std::string& path);

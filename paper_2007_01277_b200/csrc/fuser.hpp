@@ -64,6 +64,9 @@ double combined_utilization(double u1, int64_t c1, double u2, int64_t c2);
 struct FusionConfig {
   int d1 = 0, d2 = 0, d0 = 0;
   std::optional<int> reg_cap;
+  // B200 extension: per-interval register budgets (setmaxnreg; see Sm100Options), 0 = off.
+  // Exclusive with reg_cap; only the sm100 emitter honours them.
+  int regs1 = 0, regs2 = 0;
   void check(const SM& sm) const;
 };
 
@@ -114,6 +117,12 @@ struct Sm100Options {
   // JIT specialization: scalar parameters (never assigned by the kernel) whose launch
   // values are folded into the code as constants; the runtime checks them at bind time.
   std::map<std::string, ScalarVal> specialize;
+  // Per-interval register budgets (fused kernels only; 0 = off). B200 mechanics: the kernel
+  // is compiled with __maxnreg__(launch) where launch * d0 >= regs1 * d1 + regs2 * d2, and
+  // each interval re-sizes its warpgroups' allocation on entry with setmaxnreg.dec/.inc, so
+  // the two constituents no longer share one register count (the reference's single
+  // reg_cap, machine.cpp:269-283). Needs warpgroup-aligned intervals (d1, d2 % 128 == 0).
+  int regs1 = 0, regs2 = 0;
 };
 
 struct Sm100Param {
@@ -133,7 +142,15 @@ struct Sm100Kernel {
   int64_t smem_bytes = 0;  // dynamic shared memory
   std::vector<Sm100Param> params;
   std::vector<BarrierEntry> barriers;
+  // setmaxnreg budgets: per-thread registers at launch (the pool is launch_regs * threads)
+  // and per interval; 0 = not used. The runtime refuses a module whose ptxas count differs
+  // from launch_regs (an undersized pool would block setmaxnreg.inc forever).
+  int launch_regs = 0;
+  int interval_regs[2] = {0, 0};
 };
+
+// Launch register count for per-interval budgets; throws InvalidArgument / DoesNotFit.
+int interval_launch_regs(int d1, int d2, int regs1, int regs2, int64_t regs_per_sm = 65536);
 
 Sm100Kernel emit_sm100(const Fused& f, const Sm100Options& o = {});
 // One unfused kernel (normalized internally), launched 1-D with dims.count() threads.

@@ -265,6 +265,8 @@ Prepared prepare(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo
   p.opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-fmad=false"};
   if (lineinfo) p.opts.push_back("-lineinfo");
   p.source = k.source;
+  if (maxrreg && k.launch_regs > 0)
+    raise(Code::InvalidArgument, "a register cap and per-interval register budgets are exclusive");
   if (maxrreg) {
     // --maxrregcount is ignored for kernels that carry __launch_bounds__, so a register cap
     // replaces the emitted launch bounds with __maxnreg__ (the two cannot be combined).
@@ -357,6 +359,18 @@ Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) 
   cu_check(d.funcGetAttribute(&m.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, fn), "cuFuncGetAttribute");
   cu_check(d.funcGetAttribute(&m.local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, fn), "cuFuncGetAttribute");
   cu_check(d.occupancy(&m.blocks_per_sm, fn, m.threads, size_t(m.smem)), "cuOccupancyMaxActiveBlocks");
+  bool grows = k.interval_regs[0] > k.launch_regs || k.interval_regs[1] > k.launch_regs;
+  if (k.launch_regs > 0 && grows && m.regs != k.launch_regs) {
+    // setmaxnreg.inc blocks until the CTA's pool has the registers: a pool smaller than the
+    // budgets promise would hang the launch, so such a module is never handed out.
+    d.moduleUnload(mod);
+    raise(Code::Device, "'" + k.entry + "': ptxas allocated " + std::to_string(m.regs) +
+                            " registers per thread, the interval budgets need exactly " +
+                            std::to_string(k.launch_regs));
+  }
+  m.launch_regs = k.launch_regs;
+  m.interval_regs[0] = k.interval_regs[0];
+  m.interval_regs[1] = k.interval_regs[1];
   return m;
 }
 

@@ -22,6 +22,8 @@ struct Module {
   std::vector<Sm100Param> params;
   std::vector<BarrierEntry> barriers;
   std::optional<int> maxrreg;
+  int launch_regs = 0;              // per-interval budgets (setmaxnreg), 0 = off
+  int interval_regs[2] = {0, 0};
   // filled after load
   int regs = 0;
   int local_bytes = 0;  // spill / local memory per thread

@@ -33,6 +33,8 @@ class ProfilerBackend {
   // Called once with every candidate of a sweep before the first evaluate(); a backend may
   // do per-candidate work ahead of time (DeviceBackend: parallel NVRTC compilation).
   virtual void prepare(const std::vector<std::pair<Fused, FusionConfig>>& candidates) { (void)candidates; }
+  // Whether evaluate() honours per-interval register budgets (only sm100 code carries them).
+  virtual bool supports_budgets() const { return false; }
 };
 
 // Spawns `command <source-file>` and reads the first integer of its stdout (search.cpp:32-62).
@@ -40,6 +42,7 @@ class ExternalCommandBackend : public ProfilerBackend {
  public:
   explicit ExternalCommandBackend(std::string cmd, Style style = Style::Goto);
   EvalOutcome evaluate(const Fused& fused, const FusionConfig& cfg) override;
+  bool supports_budgets() const override { return style_ == Style::Sm100; }
 
  private:
   std::string cmd_;
@@ -55,6 +58,7 @@ class DeviceBackend : public ProfilerBackend {
   EvalOutcome evaluate(const Fused& fused, const FusionConfig& cfg) override;
   Resources resources(const Kernel& k, int threads) override;
   void prepare(const std::vector<std::pair<Fused, FusionConfig>>& candidates) override;
+  bool supports_budgets() const override { return true; }
   void set_specialization(std::map<std::string, ScalarVal> s) { spec_ = std::move(s); }
 
  private:
@@ -63,6 +67,8 @@ class DeviceBackend : public ProfilerBackend {
   int grid_, warmup_, reps_;
   bool flush_, measured_;
 };
+
+std::string cap_text(const FusionConfig& cfg);  // "none", "N" or "R1/R2" (budgets)
 
 struct EvalPoint {
   FusionConfig cfg;
@@ -79,7 +85,20 @@ struct SearchResult {
 struct SearchOptions {
   int granularity = 128;
   std::vector<int> extra_caps;  // C4: additional register caps evaluated per partition
+  // B200: also evaluate per-interval register budgets (setmaxnreg) for warpgroup-aligned
+  // partitions: the one-CTA-per-SM pool divided between the intervals at `budget_points`
+  // shares of the constituents' register shortfall (interval_budgets()).
+  bool interval_regs = false;
+  int budget_points = 5;
 };
+
+// Per-interval budgets for one partition: demand n1, n2 (ptxas registers of each constituent
+// alone), pool = the largest multiple-of-8 count per thread that one CTA of d1 + d2 threads
+// may hold on an SM. When both demands fit, the single point (ceil8 n1, ceil8 n2); else the
+// shortfall D is charged to interval 1 at fractions 0, 1/(p-1), ..., 1 (interval 2 takes the
+// rest of the pool), clamped to [24, 256] and deduplicated.
+std::vector<std::pair<int, int>> interval_budgets(int n1, int d1, int n2, int d2, int64_t regs_per_sm,
+                                                  int points);
 
 SearchResult search_config(const Kernel& k1, const Kernel& k2, int d0, ProfilerBackend& be, const SM& sm,
                            const SearchOptions& opt = {});

@@ -38,7 +38,7 @@ TIME_MODES = {"single": 0, "sequential": 1, "two_stream": 2}
 EXPORTS = [
     "hf_free", "hf_version", "hf_fuse", "hf_fuse_report", "hf_normalize", "hf_check", "hf_lower",
     "hf_emit_kernel", "hf_register_bound", "hf_occupancy", "hf_device_count",
-    "hf_get_device_props", "hf_build_fused", "hf_build_kernel", "hf_build_naive", "hf_build_vertical",
+    "hf_get_device_props", "hf_build_fused", "hf_build_fused_regs", "hf_build_kernel", "hf_build_naive", "hf_build_vertical",
     "hf_module_get_info",
     "hf_module_source", "hf_module_entry", "hf_module_param", "hf_module_barrier",
     "hf_module_cubin", "hf_launch", "hf_module_free", "hf_image_parse", "hf_image_merge",
@@ -74,7 +74,8 @@ class _Occ(C.Structure):
 class _ModInfo(C.Structure):
     _fields_ = [("threads", C.c_int), ("grid", C.c_int), ("smem_bytes", C.c_longlong),
                 ("regs", C.c_int), ("local_bytes", C.c_int), ("blocks_per_sm", C.c_int),
-                ("n_params", C.c_int), ("n_barriers", C.c_int)]
+                ("n_params", C.c_int), ("n_barriers", C.c_int), ("launch_regs", C.c_int),
+                ("interval_regs", C.c_int * 2)]
 
 
 class _Timing(C.Structure):
@@ -92,7 +93,8 @@ class _SearchOpts(C.Structure):
                 ("profiler_cmd", C.c_char_p), ("grid", C.c_int), ("warmup", C.c_int),
                 ("reps", C.c_int), ("flush_l2", C.c_int), ("measured_registers", C.c_int),
                 ("specialize", C.c_int), ("n_extra_caps", C.c_int), ("extra_caps", C.POINTER(C.c_int)),
-                ("out_style", C.c_int)]
+                ("out_style", C.c_int), ("interval_regs", C.c_int), ("budget_points", C.c_int),
+                ("best_regs1", C.c_int), ("best_regs2", C.c_int)]
 
 
 class _Props(C.Structure):
@@ -122,6 +124,7 @@ def _load() -> C.CDLL:
         "hf_device_count": (ip, []),
         "hf_get_device_props": (ip, [C.POINTER(_Props), E]),
         "hf_build_fused": (ip, [cp, cp, ip, ip, ip, ip, ip, vp, C.POINTER(vp), E]),
+        "hf_build_fused_regs": (ip, [cp, cp, ip, ip, ip, ip, ip, vp, C.POINTER(vp), E]),
         "hf_build_kernel": (ip, [cp, ip, ip, ip, vp, C.POINTER(vp), E]),
         "hf_build_naive": (ip, [cp, cp, ip, ip, ip, C.POINTER(vp), E]),
         "hf_build_vertical": (ip, [cp, cp, ip, vp, C.POINTER(vp), E]),
@@ -384,6 +387,8 @@ class ModuleInfo:
     blocks_per_sm: int
     n_params: int
     n_barriers: int
+    launch_regs: int = 0                 # per-interval budgets: registers per thread at launch
+    interval_regs: Tuple[int, int] = (0, 0)
 
 
 class Module:
@@ -399,6 +404,16 @@ class Module:
         h, err = C.c_void_p(), _Err()
         _check(_lib.hf_build_fused(src1.encode(), src2.encode(), d1, d2, _regcap(regcap), grid, min_blocks,
                                    specialize._h if specialize else None, C.byref(h), C.byref(err)), err)
+        return cls(h)
+
+    @classmethod
+    def fused_regs(cls, src1: str, src2: str, d1: int, d2: int, regs1: int, regs2: int, grid: int = 0,
+                   specialize: Optional["Image"] = None) -> "Module":
+        """Per-interval register budgets: interval 1 runs with regs1, interval 2 with regs2
+        registers per thread (setmaxnreg), instead of one cap for the whole fused kernel."""
+        h, err = C.c_void_p(), _Err()
+        _check(_lib.hf_build_fused_regs(src1.encode(), src2.encode(), d1, d2, regs1, regs2, grid,
+                                        specialize._h if specialize else None, C.byref(h), C.byref(err)), err)
         return cls(h)
 
     @classmethod
@@ -430,7 +445,9 @@ class Module:
     def info(self) -> ModuleInfo:
         i = _ModInfo()
         _lib.hf_module_get_info(self._h, C.byref(i))
-        return ModuleInfo(*(getattr(i, f) for f, _ in _ModInfo._fields_))
+        vals = [getattr(i, f) for f, _ in _ModInfo._fields_]
+        vals[-1] = tuple(vals[-1])
+        return ModuleInfo(*vals)
 
     @property
     def source(self) -> str:
@@ -514,11 +531,14 @@ def profile(src1: str, src2: str, d1: int, d2: int, img: Image, regcap="off", gr
 def search(src1: str, src2: str, img: Optional[Image] = None, d0: int = 1024, granularity: int = 128,
            profiler_cmd: Optional[str] = None, grid: int = 0, warmup: int = 3, reps: int = 10,
            flush_l2: bool = True, measured_registers: bool = True, extra_caps: Sequence[int] = (),
-           out_style: str = "structured", specialize: bool = False) -> dict:
+           out_style: str = "structured", specialize: bool = False, interval_regs: bool = False,
+           budget_points: int = 5) -> dict:
+    """interval_regs: also sweep per-interval register budgets (setmaxnreg) for warpgroup-
+    aligned partitions; the best point's budgets come back as "interval_regs" (or None)."""
     caps = (C.c_int * max(1, len(extra_caps)))(*extra_caps)
     o = _SearchOpts(d0, granularity, 1 if profiler_cmd else 0, _b(profiler_cmd), grid, warmup, reps,
                     int(flush_l2), int(measured_registers), int(specialize), len(extra_caps), caps,
-                    STYLES[out_style])
+                    STYLES[out_style], int(interval_regs), budget_points, 0, 0)
     d1, d2, cap, best = C.c_int(), C.c_int(), C.c_int(), C.c_longlong()
     trace, src, err = C.c_void_p(), C.c_void_p(), _Err()
     _check(_lib.hf_search(src1.encode(), src2.encode(), img._h if img else None, C.byref(o), C.byref(d1),
@@ -532,4 +552,5 @@ def search(src1: str, src2: str, img: Optional[Image] = None, d0: int = 1024, gr
         vals = line.split(",")
         rows.append({k: (v if k == "reg_cap" else float(v) if "." in v else int(v)) for k, v in zip(keys, vals)})
     return {"d1": d1.value, "d2": d2.value, "reg_cap": None if cap.value < 0 else cap.value,
+            "interval_regs": (o.best_regs1, o.best_regs2) if o.best_regs1 > 0 else None,
             "best_time": best.value, "trace_csv": csv, "trace": rows, "source": _take(src)}

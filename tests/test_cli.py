@@ -63,3 +63,48 @@ def test_lower_and_emit(tmp_path):
     assert low.returncode == 0 and "vload" not in low.stdout and "__vx0" in low.stdout
     em = run("emit", p)
     assert em.returncode == 0 and "reinterpret_cast<const float4*>(hi_x)" in em.stdout
+
+
+def test_fuse_interval_register_budgets(tmp_path):
+    """B200 extension: `--interval-regs R1,R2` emits __maxnreg__(pool) and one setmaxnreg per
+    interval; misaligned partitions, bad budgets, oversized pools and --regcap are rejected."""
+    k = os.path.join(ROOT, "paper_2007_01277_b200", "kernels", "b200")
+    bl, eh = os.path.join(k, "blake256.mk"), os.path.join(k, "ethash.mk")
+    out = tmp_path / "f.cu"
+    r = run("fuse", bl, eh, "--d1", 512, "--d2", 384, "--style", "sm100", "--sm", "b200",
+            "--interval-regs", "32,120", "-o", out)
+    assert r.returncode == 0, r.stderr
+    assert "interval_regs = 32,120 (launch 72)" in r.stdout
+    text = out.read_text()
+    assert "__maxnreg__(72)" in text and "__launch_bounds__" not in text
+    assert text.count("setmaxnreg.dec.sync.aligned.u32 32;") == 1
+    assert text.count("setmaxnreg.inc.sync.aligned.u32 120;") == 1
+    assert text.index("setmaxnreg.dec") < text.index("setmaxnreg.inc")
+    for args, code in [(("--d1", 512, "--d2", 320, "--interval-regs", "32,120"), "InvalidArgument"),
+                       (("--d1", 512, "--d2", 384, "--interval-regs", "30,120"), "InvalidArgument"),
+                       (("--d1", 512, "--d2", 384, "--interval-regs", "64,128"), "DoesNotFit"),
+                       (("--d1", 512, "--d2", 384, "--interval-regs", "32,120", "--regcap", "64"),
+                        "InvalidArgument"),
+                       (("--d1", 512, "--d2", 384, "--interval-regs", "32,120", "--style", "goto"),
+                        "InvalidArgument")]:
+        style = [] if "--style" in args else ["--style", "sm100"]
+        r = run("fuse", bl, eh, *args, *style, "--sm", "b200", "-o", out)
+        assert r.returncode == 1 and r.stderr.startswith(f"error[{code}]"), (args, r.stderr)
+
+
+def test_search_sweeps_interval_budgets_with_profiler_command(tmp_path):
+    """`search --budgets`: warpgroup-aligned partitions also get per-interval register budget
+    candidates (trace reg_cap column `R1/R2`), handed to the command as sm100 text."""
+    k = os.path.join(ROOT, "paper_2007_01277_b200", "kernels", "b200")
+    trace = tmp_path / "t.csv"
+    prof = tmp_path / "prof.sh"
+    prof.write_text("#!/bin/sh\nif grep -q setmaxnreg \"$1\"; then echo 5; else echo 11; fi\n")
+    prof.chmod(0o755)
+    r = run("search", os.path.join(k, "blake256.mk"), os.path.join(k, "ethash.mk"), "--d0", 896, "--budgets",
+            "--profiler-cmd", prof, "--trace", trace, "-o", tmp_path / "w.cu", "--style", "sm100")
+    assert r.returncode == 0, r.stderr
+    rows = [line.split(",") for line in trace.read_text().splitlines()[1:]]
+    budgets = [row[2] for row in rows if "/" in row[2]]
+    assert budgets and all(row[3] == "5" for row in rows if "/" in row[2])
+    assert "best_interval_regs = " + budgets[0] in r.stdout
+    assert "setmaxnreg" in (tmp_path / "w.cu").read_text()

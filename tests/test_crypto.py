@@ -108,3 +108,25 @@ def test_fused_crypto_pairs_on_device(gpu, a, b):
     img.download()
     assert device_outputs(img, a) == reference_outputs(a, ca, grid, 5, 1 << 28)
     assert device_outputs(img, b) == reference_outputs(b, cb, grid, 9, 1 << 28)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("a,b,d2,regs", [("sha256d", "blake2b", 512, (40, 56)),
+                                         ("blake256", "ethash", 384, (32, 120)),
+                                         ("blake256", "ethash", 512, (24, 104))])
+def test_fused_crypto_pairs_with_interval_budgets(gpu, a, b, d2, regs):
+    """Per-interval register budgets (setmaxnreg) change register allocation only: the fused
+    outputs stay bit-identical to the restatement, and ptxas allocated the promised pool."""
+    hf = gpu
+    grid = 3
+    ca, cb = (2048, 2048) if b != "ethash" else (2048, 384)
+    wa = crypto.workload(a, count=ca, grid=grid, nonce0=5, target=1 << 28)
+    wb = crypto.workload(b, count=cb, grid=grid, nonce0=9, target=1 << 28)
+    img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
+    m = hf.Module.fused_regs(src(a), src(b), crypto.THREADS[a], d2, *regs, grid=grid, specialize=img)
+    assert m.info.interval_regs == regs
+    assert "setmaxnreg" in m.source
+    m.run(img, grid)
+    img.download()
+    assert device_outputs(img, a) == reference_outputs(a, ca, grid, 5, 1 << 28)
+    assert device_outputs(img, b) == reference_outputs(b, cb, grid, 9, 1 << 28)
