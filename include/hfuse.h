@@ -200,6 +200,10 @@ const char* hf_module_source(const hf_module* m);  /* borrowed */
 const char* hf_module_entry(const hf_module* m);   /* borrowed */
 int hf_module_param(const hf_module* m, int i, const char** name, int* is_array, int* is_float,
                     int* is_written, int* is_specialized);
+/* Whether array parameter i's prior contents are observed by the kernel (loads or atomic
+ * read-modify-writes); a written array that is not read is pure output and needs no upload
+ * (the reference binds every array by name from the image, exec.cpp:190-216). */
+int hf_module_param_reads(const hf_module* m, int i, int* is_read);
 int hf_module_barrier(const hf_module* m, int i, hf_barrier* out);
 int hf_module_cubin(const hf_module* m, const void** data, size_t* size);
 /* Raw launch: args[i] points at the i-th parameter value (device pointer or scalar);

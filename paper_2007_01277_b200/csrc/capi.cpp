@@ -285,6 +285,12 @@ int hf_module_param(const hf_module* m, int i, const char** name, int* is_array,
   return HF_OK;
 }
 
+int hf_module_param_reads(const hf_module* m, int i, int* is_read) {
+  if (!m || !is_read || i < 0 || i >= int(m->m.params.size())) return to_abi(hf::Code::InvalidArgument);
+  *is_read = m->m.params[size_t(i)].read;
+  return HF_OK;
+}
+
 int hf_module_barrier(const hf_module* m, int i, hf_barrier* out) {
   if (!m || i < 0 || i >= int(m->m.barriers.size())) return to_abi(hf::Code::InvalidArgument);
   const auto& e = m->m.barriers[size_t(i)];

@@ -108,7 +108,7 @@ Sm100Kernel wrap_goto(const std::string& text, int grid) {
     if (type.empty()) continue;
     bool array = type.back() == '*';
     if (array) type.pop_back();
-    k.params.push_back(Sm100Param{name, type == "float" ? Ty::Float : Ty::Int, array, true, false, {}});
+    k.params.push_back(Sm100Param{name, type == "float" ? Ty::Float : Ty::Int, array, true, false, {}, array});
   }
   auto size_of = [&](const char* key) {
     size_t at = text.find(key);

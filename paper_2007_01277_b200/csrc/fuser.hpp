@@ -132,6 +132,7 @@ struct Sm100Param {
   bool written;             // array parameters only
   bool specialized = false; // scalar folded into the code (value below)
   ScalarVal value;
+  bool read = false;        // array parameters: prior contents are loaded (or atomically updated)
 };
 
 struct Sm100Kernel {

@@ -40,7 +40,7 @@ EXPORTS = [
     "hf_emit_kernel", "hf_register_bound", "hf_occupancy", "hf_device_count",
     "hf_get_device_props", "hf_build_fused", "hf_build_fused_regs", "hf_build_kernel", "hf_build_naive", "hf_build_vertical",
     "hf_module_get_info",
-    "hf_module_source", "hf_module_entry", "hf_module_param", "hf_module_barrier",
+    "hf_module_source", "hf_module_entry", "hf_module_param", "hf_module_param_reads", "hf_module_barrier",
     "hf_module_cubin", "hf_launch", "hf_module_free", "hf_image_parse", "hf_image_merge",
     "hf_image_materialize", "hf_image_upload", "hf_image_download", "hf_image_digest",
     "hf_image_serialize", "hf_image_count", "hf_image_entry", "hf_image_find",
@@ -133,6 +133,7 @@ def _load() -> C.CDLL:
         "hf_module_entry": (cp, [vp]),
         "hf_module_param": (ip, [vp, ip, C.POINTER(cp), C.POINTER(ip), C.POINTER(ip), C.POINTER(ip),
                                  C.POINTER(ip)]),
+        "hf_module_param_reads": (ip, [vp, ip, C.POINTER(ip)]),
         "hf_module_barrier": (ip, [vp, ip, C.POINTER(_Barrier)]),
         "hf_module_cubin": (ip, [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]),
         "hf_launch": (ip, [vp, ip, C.POINTER(vp), vp, E]),
@@ -461,10 +462,12 @@ class Module:
     def params(self) -> List[dict]:
         out = []
         for i in range(self.info.n_params):
-            n, a, f, w, sp = C.c_char_p(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+            n, a, f, w, sp, rd = C.c_char_p(), C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
             _lib.hf_module_param(self._h, i, C.byref(n), C.byref(a), C.byref(f), C.byref(w), C.byref(sp))
+            _lib.hf_module_param_reads(self._h, i, C.byref(rd))
+            # "read": an array whose prior contents the kernel observes (needs uploading)
             out.append({"name": n.value.decode(), "array": bool(a.value), "float": bool(f.value),
-                        "written": bool(w.value), "specialized": bool(sp.value)})
+                        "written": bool(w.value), "specialized": bool(sp.value), "read": bool(rd.value)})
         return out
 
     @property

@@ -6,4 +6,4 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gp
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests_rc=$?" >> gpurun_out/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke_rc=$?" >> gpurun_out/smoke.log
 timeout 1500 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench_rc=$?" >> gpurun_out/bench.err
-tail -3 gpurun_out/gpu_tests.log gpurun_out/smoke.log gpurun_out/bench.err
+for f in gpurun_out/gpu_tests.log gpurun_out/smoke.log gpurun_out/bench.err; do tail -n 3 $f; done

@@ -48,3 +48,18 @@ def test_cli_binary_present():
     exe = os.path.join(ROOT, "paper_2007_01277_b200", "bin", "hfuse")
     r = subprocess.run([exe, "nope"], capture_output=True, text=True)
     assert r.returncode == 1 and r.stderr.startswith("error[InvalidArgument]")
+
+
+def test_param_read_flags_mark_pure_outputs(hf):
+    """hf_module_param_reads: written arrays the kernel never loads (vstore/store only) are pure
+    outputs; atomically updated ones (histogram bins) and inputs are read. Compile-only on CPU."""
+    from paper_2007_01277_b200 import pairs
+    m = hf.Module.fused(pairs.source("b200", "histogram"), pairs.source("b200", "upsample"), 512, 512, grid=296)
+    p = {x["name"]: x for x in m.params if x["array"]}
+    assert p["hi_x"]["read"] and not p["hi_x"]["written"]
+    assert p["hi_out"]["read"] and p["hi_out"]["written"]      # atomic_add: read-modify-write
+    assert p["us_y"]["written"] and not p["us_y"]["read"]      # pure output: no upload needed
+    assert p["us_x"]["read"]
+    m = hf.Module.kernel(pairs.source("b200", "maxpool"), grid=296)
+    p = {x["name"]: x for x in m.params if x["array"]}
+    assert not p["mp_y"]["read"] and not p["mp_idx"]["read"] and p["mp_x"]["read"]

@@ -39,10 +39,10 @@ def test_generated_sources_are_current(tmp_path):
         assert gen() == src(kind), kind
 
 
-def reference_outputs(kind, count, grid, nonce0, target, words=None):
+def reference_outputs(kind, count, grid, nonce0, target, words=None, threads=None):
     words = words or crypto.header_words(2024, 20)
     dag = C.LazyDag(77, 1 << 10) if kind == "ethash" else None
-    return C.search_outputs(kind, words, nonce0, count, target, grid, crypto.THREADS[kind], dag=dag,
+    return C.search_outputs(kind, words, nonce0, count, target, grid, threads or crypto.THREADS[kind], dag=dag,
                             n_pages=1 << 10)
 
 
@@ -129,4 +129,4 @@ def test_fused_crypto_pairs_with_interval_budgets(gpu, a, b, d2, regs):
     m.run(img, grid)
     img.download()
     assert device_outputs(img, a) == reference_outputs(a, ca, grid, 5, 1 << 28)
-    assert device_outputs(img, b) == reference_outputs(b, cb, grid, 9, 1 << 28)
+    assert device_outputs(img, b) == reference_outputs(b, cb, grid, 9, 1 << 28, threads=d2)
