@@ -1,0 +1,35 @@
+"""Render DESIGN.md §10 tables from a bench JSON line (profiles/r01_bench_full.json)."""
+import json
+import sys
+
+d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+o = []
+o.append("| pair | grid | d1/d2 | fused µs | seq µs | 2-stream µs | speedup | roofline | naive goto fusion µs | VFuse µs |")
+o.append("|---|---|---|---|---|---|---|---|---|---|")
+for p in d["pairs"]:
+    sp = p["speedup"]
+    o.append(f"| {p['pair']} | {p['grid']} | {p['d1']}/{p['d2']}{' cap ' + str(p['reg_cap']) if p['reg_cap'] else ''} | "
+             f"{p['fused_us']:.1f} | {p['seq_us']:.1f} | {p['two_stream_us']:.1f} | "
+             f"{'**%.3f**' % sp if sp > 1.0 else '%.3f' % sp} | {p['roofline_frac']:.3f} | {p['naive_fused_us']:.1f} | {p['vertical_us']:.1f} |")
+o.append("")
+o.append(f"Geomean speedup vs min(seq, two-stream): {d['speedup_geomean']:.3f}. Step of all ten (`value`): "
+         f"{d['value']:.1f} µs fused vs {d['unfused_two_stream_step_us']:.1f} µs unfused on two streams. "
+         f"e2e (host buffers, pipelined): {d['e2e']['value'] / 1000:.1f} ms per step "
+         f"({d['e2e']['h2d_bytes_per_step'] / 1e9:.2f} GB up, {d['e2e']['d2h_bytes_per_step'] / 1e9:.2f} GB down); "
+         f"reference CPU interpreter: {d['cpu_baseline']['value'] / 1e6:.1f} s per step ({d['cpu_baseline']['cores']} processes). "
+         f"Clocks {d['clocks']['sm_mhz']:.0f}/{d['clocks']['sm_max_mhz']:.0f} MHz, reasons {d['clocks']['reasons']}.")
+o.append("")
+o.append("| crypto pair | partition | registers | fused µs | seq µs | 2-stream µs | speedup | roofline (bound) |")
+o.append("|---|---|---|---|---|---|---|---|")
+for p in d["crypto"]["c3"]:
+    regs = ("budgets %d/%d" % tuple(p["interval_regs"])) if p.get("interval_regs") else (
+        "cap %s" % p["reg_cap"] if p["reg_cap"] else "uncapped (%d)" % p["regs"])
+    r = p.get("roofline") or {}
+    o.append(f"| {p['pair']} | {p['d1']}/{p['d2']} | {regs} | {p['fused_us']:.0f} | {p['seq_us']:.0f} | "
+             f"{p['two_stream_us']:.0f} | **{p['speedup']:.3f}** | {r.get('frac', 0):.2f} issue, {r.get('alu_frac', 0):.2f} ALU pipe |")
+c4 = d["crypto"]["c4"]
+b = c4["best"]
+o.append("")
+o.append(f"C4 Upsample + BLAKE-256: best d0 {b['d0']} (Upsample {b['d1']}), reg_cap {b['reg_cap']}: {b['us']:.1f} µs vs "
+         f"{c4['seq_us']:.1f} sequential / {c4['two_stream_us']:.1f} two-stream — **{c4['speedup']:.3f}×**.")
+print("\n".join(o))
