@@ -162,6 +162,11 @@ class Checker {
         switch (Intr(e.i)) {
           case Intr::CastInt: type(e.a[0]); return Ty::Int;
           case Intr::IntRz: type(e.a[0]); return Ty::Int;
+          case Intr::Acquire:
+          case Intr::Relaxed:
+            if (e.a[0].k != EK::Index)
+              raise(Code::TypeMismatch, std::string(intr_name(Intr(e.i))) + " takes an array element", e.a[0].pos);
+            return type(e.a[0]);
           case Intr::CastFloat: type(e.a[0]); return Ty::Float;
           case Intr::Fmaxf:
             type(e.a[0]);

@@ -75,6 +75,8 @@ struct GotoPrinter {
         switch (Intr(e.i)) {
           case Intr::CastInt:
           case Intr::IntRz: return "(int)(" + ex(e.a[0]) + ")";
+          case Intr::Acquire:
+          case Intr::Relaxed: return ex(e.a[0]);
           case Intr::CastFloat: return "(float)(" + ex(e.a[0]) + ")";
           default: {
             std::string t = std::string(intr_name(Intr(e.i))) + "(";

@@ -560,6 +560,20 @@ class Parser {
           }
           if ((at_ident("vload") || at_ident("vstore")) && at(T::LParen, 1))
             return vector_access(p);
+          if (at_ident("atomic_add_release") && at(T::LParen, 1)) {
+            // release-ordered atomic add: earlier writes of this thread are visible to whoever
+            // observes the update (load_acquire) -- the inter-block hand-off without fence()
+            next();
+            want(T::LParen);
+            s.k = SK::Atomic;
+            s.bid = 1;
+            lvalue(s);
+            want(T::Comma);
+            s.val.push_back(expr());
+            want(T::RParen);
+            want(T::Semi);
+            return s;
+          }
           if ((at_ident("fence") || at_ident("warp_sync")) && at(T::LParen, 1) && at(T::RParen, 2)) {
             s.k = next().text == "fence" ? SK::Fence : SK::WarpSync;
             next();
@@ -828,6 +842,8 @@ class Parser {
           else if (b200() && n.text == "fshr") w = Intr::Fshr;
           else if (b200() && n.text == "fshl") w = Intr::Fshl;
           else if (b200() && n.text == "int_rz") w = Intr::IntRz;
+          else if (b200() && n.text == "load_acquire") w = Intr::Acquire;
+          else if (b200() && n.text == "load_relaxed") w = Intr::Relaxed;
           if (w) {
             std::vector<Expr> a = args();
             if (int(a.size()) != intr_arity(*w))

@@ -39,12 +39,16 @@ const char* intr_name(Intr i) {
     case Intr::Fshr: return "fshr";
     case Intr::Fshl: return "fshl";
     case Intr::IntRz: return "int_rz";
+    case Intr::Acquire: return "load_acquire";
+    case Intr::Relaxed: return "load_relaxed";
   }
   return "?";
 }
 
 int intr_arity(Intr i) {
-  if (i == Intr::CastInt || i == Intr::CastFloat || i == Intr::IntRz) return 1;
+  if (i == Intr::CastInt || i == Intr::CastFloat || i == Intr::IntRz || i == Intr::Acquire ||
+      i == Intr::Relaxed)
+    return 1;
   if (i == Intr::Fshr || i == Intr::Fshl) return 3;
   return 2;
 }
@@ -500,7 +504,7 @@ struct MkPrinter {
         break;
       case SK::Atomic:
         pad(ind);
-        o += "atomic_add(";
+        o += s.bid == 1 ? "atomic_add_release(" : "atomic_add(";
         lvalue(s);
         o += ", ";
         expr(s.val[0]);

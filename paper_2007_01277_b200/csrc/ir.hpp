@@ -68,6 +68,8 @@ enum class Intr : uint8_t {
   Fshr,   // fshr(lo, hi, n): low word of (hi:lo) >> (n & 31)   (64-bit rotates in 32-bit halves)
   Fshl,   // fshl(lo, hi, n): high word of (hi:lo) << (n & 31)
   IntRz,  // int_rz(x): int(x) for |x| < 2^31 (device: one cvt.rzi.s32); outside that range undefined
+  Acquire,  // load_acquire(a[i]): a[i] read with gpu-scope acquire (pairs with atomic_add_release)
+  Relaxed,  // load_relaxed(a[i]): gpu-scope strong read, no ordering (a later fence() acquires)
 };
 const char* intr_name(Intr i);
 int intr_arity(Intr i);
@@ -104,7 +106,7 @@ struct Stmt {
   std::vector<Stmt> body, alt;    // If then/else; loop body
   std::vector<Stmt> init, step;   // For header (one statement each)
   bool has_alt = false;
-  int bid = 0, bcount = 0;        // BarSync
+  int bid = 0, bcount = 0;        // BarSync; Atomic: bid 1 = atomic_add_release (MK+)
   int unroll = 0;                 // For (MK+): 0 = no hint, -1 = `unroll`, N = `unroll N`
 };
 using Block = std::vector<Stmt>;

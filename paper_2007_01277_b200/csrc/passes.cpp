@@ -645,6 +645,8 @@ struct Lowerer {
     const Expr& n = c.a.size() > 1 ? c.a[1] : c.a[0];
     switch (Intr(c.i)) {
       case Intr::IntRz: return intrin(Intr::CastInt, {x});
+      case Intr::Acquire:
+      case Intr::Relaxed: return x;  // the interpreter is sequentially consistent
       case Intr::ShrU: return shr_u(x, n);
       case Intr::Rotr: {
         Expr left = binary(Bin::Shl, x, binary(Bin::Sub, lit(32), binary(Bin::And, n, lit(31))));
@@ -707,6 +709,7 @@ struct Lowerer {
     c.body = block(c.body);
     c.alt = block(c.alt);
     if (c.k == SK::Fence) return;     // the interpreter is sequentially consistent
+    if (c.k == SK::Atomic) c.bid = 0;  // atomic_add_release -> atomic_add (same reason)
     if (c.k == SK::WarpSync) return;  // ... and runs each warp in lock step
     if (c.k == SK::VLoad || c.k == SK::VStore) {
       int id = counter++;

@@ -37,17 +37,17 @@ class Member:
 BN_SLOTS = 64  # >= grid / C + 2 for every grid the bench tries (C = 256: grids up to 15,872)
 
 
-def _bn(N: int, C: int, HW: int) -> Callable[[int], Workload]:
+def _bn(N: int, C: int, HW: int, slots: int = BN_SLOTS) -> Callable[[int], Workload]:
     def make(seed: int = 0) -> Workload:
         n = N * C * HW
         # + the B200 form's grid-balancing workspace: BN_SLOTS partial (count, mean, M2) slots
         # per channel and one arrival counter per channel (zero between launches)
         img = (f"array bn_x float32 {n} seed {1 + seed} uniform -1 1\n"
                f"array bn_stats float32 {2 * C} zero\n"
-               f"array bn_pn int32 {BN_SLOTS * C} zero\narray bn_pa float32 {BN_SLOTS * C} zero\n"
-               f"array bn_pm float32 {BN_SLOTS * C} zero\narray bn_cnt int32 {C} zero\n"
+               f"array bn_pn int32 {slots * C} zero\narray bn_pa float32 {slots * C} zero\n"
+               f"array bn_pm float32 {slots * C} zero\narray bn_cnt int32 {C} zero\n"
                f"scalar bn_N int32 {N}\nscalar bn_C int32 {C}\nscalar bn_HW int32 {HW}\n"
-               f"scalar bn_P int32 {BN_SLOTS}\n")
+               f"scalar bn_P int32 {slots}\n")
         return Workload(img, 4 * n + 8 * C, f"bn_stats x[{N},{C},{HW}] fp32")
     return make
 

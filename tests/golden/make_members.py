@@ -25,6 +25,7 @@ from paper_2007_01277_b200 import pairs  # noqa: E402
 GRID = 4
 SPLITS = [256, 512, 768]
 BN_GRIDS = [3, 7, 16, 37]
+WARP_SLOTS = 256  # >= (37 / 8 + 2) * 32
 OUTPUTS = {"bn": ["bn_stats"], "hist": ["hi_out"], "maxpool": ["mp_y", "mp_idx"], "upsample": ["us_y"],
            "im2col": ["ic_col"]}
 
@@ -83,6 +84,19 @@ def main():
             for g in BN_GRIDS:
                 dig, _, _ = oracle.ref_run("run", bal, "--mem", img, "--grid", g)
                 out["bn_grids"][size][str(g)] = dig
+        # warp-level hand-off form (atomic_add_release / load_relaxed): WARP_SLOTS partial slots
+        warp = os.path.join(d, "bn_warp.mk")
+        with open(warp, "w") as f:
+            f.write(hf.lower(pairs.source("b200", "batchnorm_warp")))
+        out["bn_warp_grids"] = {}
+        for size, dims in (("tiny", (1, 3, 16)), ("parity", (2, 8, 56 * 56))):
+            img = os.path.join(d, f"bn_{size}_warp.img")
+            with open(img, "w") as f:
+                f.write(pairs._bn(*dims, slots=WARP_SLOTS)(0).image)
+            out["bn_warp_grids"][size] = {}
+            for g in BN_GRIDS:
+                dig, _, _ = oracle.ref_run("run", warp, "--mem", img, "--grid", g)
+                out["bn_warp_grids"][size][str(g)] = dig
     with open(os.path.join(HERE, "members.json"), "w") as f:
         json.dump(out, f, sort_keys=True)
     print("members fixtures written")

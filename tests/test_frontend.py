@@ -118,3 +118,38 @@ def test_member_kernels_parse_and_lower(hf):
             src = pairs.source(form, m.stem)
             assert hf.check(src).startswith("ok: 1 kernel(s)")
             assert hf.check(hf.lower(src), strict=True).startswith("ok: 1 kernel(s)")
+
+
+HANDOFF = """kernel k(int part[], int cnt[], int out[]) dims (64, 1, 1) {
+  shared int s[2];
+  int lane = threadIdx.x % 32;
+  if (lane == 0) {
+    part[threadIdx.x / 32] = threadIdx.x + 5;
+    atomic_add_release(cnt[0], 1);
+    if (load_relaxed(cnt[0]) == 2) {
+      fence();
+      out[0] = part[0] + load_acquire(part[1]);
+    }
+  }
+}
+"""
+
+
+def test_release_acquire_handoff_constructs(hf):
+    """MK+ inter-block hand-off: atomic_add_release / load_relaxed / load_acquire print back as
+    written, lower to atomic_add / plain loads for the (sequentially consistent) interpreter,
+    and emit red.release / ld.relaxed / ld.acquire at gpu scope for sm_100a."""
+    assert hf.check(HANDOFF).startswith("ok")
+    low = hf.lower(HANDOFF)
+    assert "atomic_add(cnt[0], 1);" in low and "release" not in low and "load_" not in low
+    assert hf.check(low, strict=True).startswith("ok")
+    cu = hf.emit_kernel(HANDOFF)
+    assert "hf_red_release(&cnt[0], 1);" in cu
+    assert "hf_ld_relaxed(&cnt[0])" in cu and "hf_ld_acquire(&part[1])" in cu
+    assert "red.release.gpu.global.add.s32" in cu and "ld.acquire.gpu.global.s32" in cu
+    for bad, code in [("a[0] = load_acquire(3);", "TypeMismatch"),
+                      ("atomic_add_release(s[0], 1);", "InvalidArgument")]:
+        src = "kernel k(int a[]) dims (32, 1, 1) {\n  shared int s[2];\n  " + bad + "\n}\n"
+        with pytest.raises(hf.HFuseError) as e:
+            hf.emit_kernel(src) if code == "InvalidArgument" else hf.check(src)
+        assert e.value.name == code

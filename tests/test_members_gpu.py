@@ -175,3 +175,18 @@ def test_full_size_bn_any_grid(gpu, grid):
         mod.run(img, grid)
     img.download()
     check_full("bn", img)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grid", [3, 7, 16, 37])
+@pytest.mark.parametrize("size,dims", [("tiny", (1, 3, 16)), ("parity", (2, 8, 56 * 56))])
+def test_warp_handoff_bn_matches_interpreter(gpu, size, dims, grid):
+    """The warp-level hand-off BatchNorm (red.release.gpu counters, ld.relaxed re-read, fenced
+    last-warp merge) equals the interpreter bit for bit, and twice in a row (counters cleared)."""
+    hf = gpu
+    mod = hf.Module.kernel(pairs.source("b200", "batchnorm_warp"), grid=grid)
+    img = hf.Image(pairs._bn(*dims, slots=256)(0).image).upload()
+    for _ in range(2):
+        mod.run(img, grid)
+        img.download()
+        assert img.digest_hex() == G["bn_warp_grids"][size][str(grid)]
