@@ -9,7 +9,8 @@ sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")
 from paper_2007_01277_b200 import hfuse as hf  # noqa: E402
 from paper_2007_01277_b200 import pairs as P  # noqa: E402
 
-cur = P.source("b200", "upsample")
+# the per-thread-store form these variants rewrite (superseded: kernels/b200/upsample.mk)
+cur = open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "upsample_v1.mk")).read()
 variants = {
     "current": cur,
     "split_halves": cur.replace("vstore(us_y, 2 * t, y0, y1, y2, y3);", "vstore(us_y, t, y0, y1, y2, y3);")
