@@ -315,6 +315,7 @@ int hf_launch(const hf_module* m, int grid, void** args, void* stream, hf_error*
       if (!same)
         hf::raise(hf::Code::InvalidArgument, "module is specialized for a different value of scalar '" + p.name + "'");
     }
+    hf::rt::check_requires(m->m, args);
     hf::rt::launch_raw(m->m, grid > 0 ? grid : m->m.grid, args, stream);
   });
 }

@@ -343,6 +343,28 @@ class Parser {
 
   void annotations(const std::vector<Tok>& anns, Kernel& k) {
     for (const auto& a : anns) {
+      size_t b = a.text.find_first_not_of(" \t");
+      if (b200() && b != std::string::npos && a.text.compare(b, 8, "requires") == 0 &&
+          (b + 8 == a.text.size() || std::isspace(static_cast<unsigned char>(a.text[b + 8])))) {
+        // MK+ `//@ requires EXPR`: a launch precondition over scalar int parameters
+        Parser sub(a.text.substr(b + 8), dialect_);
+        Expr e = sub.expr();
+        if (!sub.at(T::End)) raise(Code::Syntax, "trailing text after the requires expression", a.pos);
+        std::string bad;
+        walk_expr(e, [&](const Expr& x) {
+          if (x.k == EK::Var) {
+            bool ok = false;
+            for (const auto& p : k.params) ok |= p.name == x.s && !p.array && p.ty == Ty::Int;
+            if (!ok && bad.empty()) bad = "'" + x.s + "' is not a scalar int parameter";
+          } else if (x.k != EK::Int && x.k != EK::Unary && x.k != EK::Binary &&
+                     !(x.k == EK::Intrin && (Intr(x.i) == Intr::Min || Intr(x.i) == Intr::Max))) {
+            if (bad.empty()) bad = "only scalar int arithmetic is allowed";
+          }
+        });
+        if (!bad.empty()) raise(Code::TypeMismatch, "requires: " + bad, a.pos);
+        k.reqs.push_back(std::move(e));
+        continue;
+      }
       std::istringstream in(a.text);
       std::string item;
       while (in >> item) {

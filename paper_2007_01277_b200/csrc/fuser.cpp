@@ -186,6 +186,8 @@ Fused fuse(const Kernel& k1, const Kernel& k2, int d1, int d2, const SM& sm) {
   f.k2_name = k2.name;
   f.cfg = cfg;
   f.grid = k1.grid;
+  f.reqs = k1.reqs;
+  f.reqs.insert(f.reqs.end(), k2.reqs.begin(), k2.reqs.end());
   f.dims1 = partition_dims(k1, d1);
   f.dims2 = partition_dims(k2, d2);
 
@@ -337,6 +339,7 @@ Kernel Fused::to_kernel() const {
   k.shared = shared;
   k.grid = grid;
   k.regcap = cfg.reg_cap;
+  k.reqs = reqs;
   for (const auto& s : prologue_decls) k.body.push_back(s);
   for (const auto& s : decls) k.body.push_back(s);
   for (const auto& s : prologue) k.body.push_back(s);

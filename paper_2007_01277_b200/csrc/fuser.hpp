@@ -88,6 +88,7 @@ struct Fused {
   FusionConfig cfg;
   int grid = 1;
   Dims dims1, dims2;
+  std::vector<Expr> reqs;  // MK+ launch preconditions of both constituents
 
   Kernel to_kernel() const;  // canonical structured form (valid Mini-Kernel)
 };
@@ -148,6 +149,7 @@ struct Sm100Kernel {
   // from launch_regs (an undersized pool would block setmaxnreg.inc forever).
   int launch_regs = 0;
   int interval_regs[2] = {0, 0};
+  std::vector<Expr> reqs;  // `//@ requires` preconditions, checked when a launch binds scalars
 };
 
 // Launch register count for per-interval budgets; throws InvalidArgument / DoesNotFit.

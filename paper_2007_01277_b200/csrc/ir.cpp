@@ -1,5 +1,6 @@
 #include "ir.hpp"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -567,6 +568,11 @@ struct MkPrinter {
     if (k.regs) ann += " regs=" + std::to_string(*k.regs);
     if (k.regcap) ann += " regcap=" + std::to_string(*k.regcap);
     if (!ann.empty()) o += "//@" + ann + "\n";
+    for (const auto& r : k.reqs) {
+      o += "//@ requires ";
+      expr(r);
+      o += "\n";
+    }
     o += "kernel " + k.name + "(";
     params(k.params);
     o += ") dims (" + std::to_string(k.dims.x) + ", " + std::to_string(k.dims.y) + ", " +
@@ -622,6 +628,55 @@ std::string print_mk(const Program& prog) {
     out += print_mk(k);
   }
   return out;
+}
+
+std::optional<int32_t> eval_scalar_int(const Expr& e,
+                                       const std::function<std::optional<int32_t>(const std::string&)>& value) {
+  auto w = [](int64_t v) { return int32_t(uint32_t(uint64_t(v))); };
+  switch (e.k) {
+    case EK::Int: return e.i;
+    case EK::Var: return value(e.s);
+    case EK::Unary: {
+      auto a = eval_scalar_int(e.a[0], value);
+      if (!a) return std::nullopt;
+      if (Un(e.i) == Un::Not) return *a == 0 ? 1 : 0;
+      return w(-int64_t(*a));
+    }
+    case EK::Binary: {
+      auto a = eval_scalar_int(e.a[0], value), b = eval_scalar_int(e.a[1], value);
+      if (!a || !b) return std::nullopt;
+      int64_t x = *a, y = *b;
+      switch (Bin(e.i)) {
+        case Bin::Add: return w(x + y);
+        case Bin::Sub: return w(x - y);
+        case Bin::Mul: return w(x * y);
+        case Bin::Div: return y == 0 ? std::nullopt : std::optional<int32_t>(y == -1 ? w(-x) : int32_t(x / y));
+        case Bin::Mod: return y == 0 ? std::nullopt : std::optional<int32_t>(y == -1 ? 0 : int32_t(x % y));
+        case Bin::Shl: return w(int64_t(uint32_t(*a) << (y & 31)));
+        case Bin::Shr: return int32_t(*a >> (y & 31));
+        case Bin::And: return *a & *b;
+        case Bin::Or: return *a | *b;
+        case Bin::Xor: return *a ^ *b;
+        case Bin::Lt: return x < y;
+        case Bin::Le: return x <= y;
+        case Bin::Gt: return x > y;
+        case Bin::Ge: return x >= y;
+        case Bin::Eq: return x == y;
+        case Bin::Ne: return x != y;
+        case Bin::LAnd: return (x != 0) && (y != 0);
+        case Bin::LOr: return (x != 0) || (y != 0);
+      }
+      return std::nullopt;
+    }
+    case EK::Intrin: {
+      Intr i = Intr(e.i);
+      if (i != Intr::Min && i != Intr::Max) return std::nullopt;
+      auto a = eval_scalar_int(e.a[0], value), b = eval_scalar_int(e.a[1], value);
+      if (!a || !b) return std::nullopt;
+      return i == Intr::Min ? std::min(*a, *b) : std::max(*a, *b);
+    }
+    default: return std::nullopt;
+  }
 }
 
 }  // namespace hf

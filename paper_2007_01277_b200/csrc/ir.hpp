@@ -141,8 +141,18 @@ struct Kernel {
   int grid = 1;                 // //@ grid=
   std::optional<int> regs;      // //@ regs=
   std::optional<int> regcap;    // //@ regcap=
+  // MK+ `//@ requires EXPR`: launch preconditions over scalar int parameters (e.g. a vector
+  // width dividing a row length). Checked by the runtime when a launch binds its scalars;
+  // dropped by the lowering to plain Mini-Kernel (the reference has no such annotation).
+  std::vector<Expr> reqs;
   Pos pos;
 };
+
+// Host evaluation of an int expression over named scalars with the interpreter's pinned
+// integer semantics (exec.cpp:26-48); nullopt when it names an unknown scalar, divides by zero
+// or uses a construct outside scalar int arithmetic.
+std::optional<int32_t> eval_scalar_int(const Expr& e,
+                                       const std::function<std::optional<int32_t>(const std::string&)>& value);
 
 struct Func {
   std::string name;

@@ -744,6 +744,7 @@ Kernel downlower(const Kernel& k) {
   for (const auto& sh : k.shared) l.arrays[sh.name] = sh.ty;
   Kernel out = k;
   out.body = l.block(k.body);
+  out.reqs.clear();  // `//@ requires` is MK+ only (the reference rejects unknown annotations)
   return out;
 }
 

@@ -339,6 +339,7 @@ Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) 
   m.smem = k.smem_bytes;
   m.params = k.params;
   m.barriers = k.barriers;
+  m.reqs = k.reqs;
   m.maxrreg = maxrreg;
   Prepared p = prepare(k, maxrreg, lineinfo);
   m.source = p.source;
@@ -441,6 +442,31 @@ void launch_raw(const Module& m, int grid, void** args, void* stream) {
            "cuLaunchKernel");
 }
 
+void check_requires(const Module& m, void* const* args) {
+  if (m.reqs.empty()) return;
+  auto value = [&](const std::string& n) -> std::optional<int32_t> {
+    for (size_t i = 0; i < m.params.size(); ++i) {
+      const Sm100Param& p = m.params[i];
+      if (p.name != n || p.array || p.ty != Ty::Int) continue;
+      if (p.specialized) return p.value.i;
+      return *static_cast<const int32_t*>(args[i]);
+    }
+    return std::nullopt;
+  };
+  for (const auto& r : m.reqs) {
+    auto v = eval_scalar_int(r, value);
+    if (!v || *v == 0) {
+      std::string got;
+      walk_expr(r, [&](const Expr& x) {
+        if (x.k != EK::Var) return;
+        auto xv = value(x.s);
+        got += (got.empty() ? "" : ", ") + x.s + " = " + (xv ? std::to_string(*xv) : "?");
+      });
+      raise(Code::InvalidArgument, "kernel '" + m.entry + "' requires " + print_expr(r) + " (" + got + ")");
+    }
+  }
+}
+
 namespace {
 struct Bound {
   std::vector<void*> ptrs;
@@ -476,6 +502,7 @@ Bound bind(const Module& m, Image& img) {
       b.args[i] = &b.cells[i];
     }
   }
+  check_requires(m, b.args.data());
   return b;
 }
 }  // namespace

@@ -22,6 +22,7 @@ struct Module {
   std::vector<Sm100Param> params;
   std::vector<BarrierEntry> barriers;
   std::optional<int> maxrreg;
+  std::vector<Expr> reqs;           // `//@ requires` launch preconditions
   int launch_regs = 0;              // per-interval budgets (setmaxnreg), 0 = off
   int interval_regs[2] = {0, 0};
   // filled after load
@@ -65,6 +66,9 @@ void* device_ptr(Image& img, const std::string& name);
 // Binds parameters by name from the image (exec.cpp:190-216) and launches.
 void launch(const Module& m, Image& img, int grid, void* stream = nullptr);
 void launch_raw(const Module& m, int grid, void** args, void* stream = nullptr);
+// Throws InvalidArgument when a `//@ requires` precondition is false for these scalar values
+// (args[i] points at parameter i's value; specialized parameters use their folded value).
+void check_requires(const Module& m, void* const* args);
 
 struct Timing {
   double median_us = 0, min_us = 0, mean_us = 0, max_us = 0;

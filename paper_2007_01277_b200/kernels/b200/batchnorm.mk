@@ -11,6 +11,7 @@
 // warp-shuffle Chan tree and a shared-memory stage per warp.
 // Grid-stride over channels, so any common grid works.
 //@ grid=256
+//@ requires bn_HW % 4 == 0
 kernel bn_stats(float bn_x[], float bn_stats[], int bn_N, int bn_C, int bn_HW) dims (1024, 1, 1) {
   shared int bn_sn[32];
   shared float bn_savg[32];

@@ -24,6 +24,7 @@
 // Requires HW % 4 == 0, C * N * HW / 4 >= gridDim.x and bn_P >= gridDim.x / C + 2.
 // regcap 32 keeps two 1024-thread blocks per SM (the rare merge path may spill).
 //@ grid=256 regcap=32
+//@ requires bn_HW % 4 == 0
 kernel bn_stats_balanced(float bn_x[], float bn_stats[], int bn_pn[], float bn_pa[], float bn_pm[], int bn_cnt[],
                 int bn_N, int bn_C, int bn_HW, int bn_P) dims (1024, 1, 1) {
   shared int bn_sn[32];

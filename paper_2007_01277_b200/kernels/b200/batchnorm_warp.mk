@@ -27,6 +27,7 @@
 //    and clears bn_cnt[c] for the next launch.
 // Requires HW % 4 == 0, T >= gridDim.x and bn_P >= (gridDim.x / C + 2) * blockDim / 32.
 //@ grid=296 regcap=32
+//@ requires bn_HW % 4 == 0
 kernel bn_stats(float bn_x[], float bn_stats[], int bn_pn[], float bn_pa[], float bn_pm[], int bn_cnt[],
                 int bn_N, int bn_C, int bn_HW, int bn_P) dims (1024, 1, 1) {
   int tid = threadIdx.x;

@@ -4,8 +4,9 @@
 // int((v + 4) * 8) is bit-identical to the division form (both scalings are exact); inside the
 // range guard (v + 4) * 8 is in [0, 64], so the conversion is int_rz (one cvt.rzi.s32 instead
 // of the general int() lowering, which goes through int64 for |x| >= 2^31).
-// B200 mechanics: four 128-bit coalesced loads in flight per thread per iteration
-// (n % 4 == 0; tail loads clamped in bounds and masked), warp-private shared-memory bins
+// B200 mechanics: four 128-bit coalesced loads in flight per thread per iteration over the
+// first 4 * (n / 4) values (tail loads clamped in bounds and masked; the n % 4 trailing
+// values are binned by block 0 with scalar loads, so any n works), warp-private shared-memory bins
 // (32 x 64 counters: contention only inside a warp), one global atomic per bin per block.
 //@ grid=256
 kernel hist(float hi_x[], int hi_out[], int hi_n) dims (1024, 1, 1) {
@@ -79,6 +80,13 @@ kernel hist(float hi_x[], int hi_out[], int hi_n) dims (1024, 1, 1) {
       if (v15 >= -4.0 && v15 <= 4.0) {
         atomic_add(hi_bins[wb + min(int_rz((v15 + 4.0) * 8.0), 63)], 1);
       }
+    }
+  }
+  // the n % 4 trailing values the vector loop does not cover: block 0, one per thread
+  if (blockIdx.x == 0 && tid < hi_n - 4 * n4) {
+    v0 = hi_x[4 * n4 + tid];
+    if (v0 >= -4.0 && v0 <= 4.0) {
+      atomic_add(hi_bins[wb + min(int_rz((v0 + 4.0) * 8.0), 63)], 1);
     }
   }
   syncthreads();

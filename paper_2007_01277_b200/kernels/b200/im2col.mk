@@ -6,6 +6,7 @@
 // (c, kh, kw) row are contiguous across consecutive threads. Same values as the reference
 // form (pure data movement).
 //@ grid=256
+//@ requires ic_W % 4 == 0
 kernel im2col(float ic_x[], float ic_col[], int ic_NC, int ic_H, int ic_W) dims (1024, 1, 1) {
   int nthr = blockDim.x * blockDim.y * blockDim.z;
   int w4 = ic_W / 4;

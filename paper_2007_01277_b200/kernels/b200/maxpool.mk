@@ -6,6 +6,7 @@
 // input window is read with 9 loads instead of 36, and stores 4 values + 4 indices with
 // two 128-bit stores.
 //@ grid=256
+//@ requires mp_H == 2 * mp_OH && mp_W == 2 * mp_OW && mp_W % 8 == 0
 kernel maxpool(float mp_x[], float mp_y[], int mp_idx[], int mp_NC, int mp_H, int mp_W, int mp_OH, int mp_OW) dims (1024, 1, 1) {
   int nthr = blockDim.x * blockDim.y * blockDim.z;
   int ow4 = mp_OW / 4;

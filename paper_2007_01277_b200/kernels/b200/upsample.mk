@@ -14,6 +14,7 @@
 // of a row (full 32-B sectors per thread pair, no shared-memory staging; the previous form
 // staged through shared memory and was L1-throughput bound, ncu 91.5 %).
 //@ grid=256
+//@ requires us_OH == 2 * us_IH && us_OW == 2 * us_IW && us_IW % 2 == 0
 kernel upsample(float us_x[], float us_y[], int us_NC, int us_IH, int us_IW, int us_OH, int us_OW) dims (1024, 1, 1) {
   int nthr = blockDim.x * blockDim.y * blockDim.z;
   int ow4 = us_OW / 4;

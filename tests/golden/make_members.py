@@ -26,6 +26,7 @@ GRID = 4
 SPLITS = [256, 512, 768]
 BN_GRIDS = [3, 7, 16, 37]
 WARP_SLOTS = 256  # >= (37 / 8 + 2) * 32
+RAGGED = [1, 3, 1001, 4099]
 OUTPUTS = {"bn": ["bn_stats"], "hist": ["hi_out"], "maxpool": ["mp_y", "mp_idx"], "upsample": ["us_y"],
            "im2col": ["ic_col"]}
 
@@ -75,6 +76,8 @@ def main():
         bal = os.path.join(d, "batchnorm_balanced_b200.mk")
         with open(bal, "w") as f:
             f.write(hf.lower(pairs.source("b200", "batchnorm_balanced")))
+        with open(os.path.join(d, "hist_ref.mk"), "w") as f:
+            f.write(pairs.source("ref", "histogram"))
         out["bn_grids"] = {}
         for size in ("tiny", "parity"):
             img = os.path.join(d, f"bn_{size}_grids.img")
@@ -97,6 +100,17 @@ def main():
             for g in BN_GRIDS:
                 dig, _, _ = oracle.ref_run("run", warp, "--mem", img, "--grid", g)
                 out["bn_warp_grids"][size][str(g)] = dig
+        # ragged histogram lengths (n % 4 != 0, n < 4): the reference form and the B200 form
+        out["hist_ragged"] = {}
+        for n in RAGGED:
+            img = os.path.join(d, f"hist_{n}.img")
+            with open(img, "w") as f:
+                f.write(pairs._hist(n, -4.5, 4.5)(0).image)
+            for g in (4, 37):
+                dig_ref, _, _ = oracle.ref_run("run", os.path.join(d, "hist_ref.mk"), "--mem", img, "--grid", g)
+                dig_b200, _, _ = oracle.ref_run("run", lowered["hist"], "--mem", img, "--grid", g)
+                assert dig_ref == dig_b200, (n, g)
+                out["hist_ragged"][f"{n}/{g}"] = dig_b200
     with open(os.path.join(HERE, "members.json"), "w") as f:
         json.dump(out, f, sort_keys=True)
     print("members fixtures written")

@@ -5,6 +5,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 from conftest import ROOT
 
 HEADER = os.path.join(ROOT, "include", "hfuse.h")
@@ -63,3 +65,33 @@ def test_param_read_flags_mark_pure_outputs(hf):
     m = hf.Module.kernel(pairs.source("b200", "maxpool"), grid=296)
     p = {x["name"]: x for x in m.params if x["array"]}
     assert not p["mp_y"]["read"] and not p["mp_idx"]["read"] and p["mp_x"]["read"]
+
+
+def test_requires_annotation_checked_before_launch(hf):
+    """`//@ requires` (MK+): printed back, dropped by the lowering, carried into fused kernels,
+    refused at hf_launch when false (checked before the device is touched, so this runs on CPU)
+    and at build time when every scalar it names is JIT-specialized."""
+    from paper_2007_01277_b200 import pairs
+    bn, up = pairs.source("b200", "batchnorm"), pairs.source("b200", "upsample")
+    assert "requires" not in hf.lower(bn)
+    src, _ = hf.fuse(bn, up, 512, 512, style="structured", sm="b200")
+    assert "//@ requires bn_HW % 4 == 0\n" in src and "//@ requires us_OH == 2 * us_IH" in src
+    m = hf.Module.fused(bn, up, 512, 512, grid=8)
+    args = {p["name"]: 0 for p in m.params}
+    args.update(bn_N=2, bn_C=3, bn_HW=18, us_NC=1, us_IH=4, us_IW=4, us_OH=8, us_OW=8)
+    with pytest.raises(hf.HFuseError) as e:
+        m.launch(args, grid=8)
+    assert e.value.name == "InvalidArgument" and "requires bn_HW % 4 == 0 (bn_HW = 18)" in str(e.value)
+    args["bn_HW"] = 16
+    with pytest.raises(hf.HFuseError) as e:   # precondition holds: now it is the missing GPU
+        m.launch(args, grid=8)
+    assert e.value.name != "InvalidArgument"
+    bad = hf.Image(pairs._bn(2, 3, 18)(0).image)
+    with pytest.raises(hf.HFuseError) as e:
+        hf.Module.kernel(bn, grid=4, specialize=bad)
+    assert e.value.name == "InvalidArgument" and "specialized" in str(e.value)
+    for text, code in [("//@ requires bn_x[0] == 1\n", "TypeMismatch"), ("//@ requires nope > 1\n", "TypeMismatch"),
+                       ("//@ requires bn_HW %\n", "Syntax")]:
+        with pytest.raises(hf.HFuseError) as e:
+            hf.check(text + bn[bn.index("kernel bn_stats"):])
+        assert e.value.name == code, text

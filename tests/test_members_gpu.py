@@ -190,3 +190,33 @@ def test_warp_handoff_bn_matches_interpreter(gpu, size, dims, grid):
         mod.run(img, grid)
         img.download()
         assert img.digest_hex() == G["bn_warp_grids"][size][str(grid)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 3, 1001, 4099])
+@pytest.mark.parametrize("grid", [4, 37])
+def test_hist_ragged_lengths(gpu, n, grid):
+    """n % 4 != 0 (and n < 4): the B200 Hist bins the trailing values too, equal to the
+    reference form on the interpreter (fixture) and to the C restatement."""
+    hf = gpu
+    w = pairs._hist(n, -4.5, 4.5)(0)
+    img = hf.Image(w.image).upload()
+    hf.Module.kernel(pairs.source("b200", "histogram"), grid=grid).run(img, grid)
+    img.download()
+    assert img.digest_hex() == G["hist_ragged"][f"{n}/{grid}"]
+    arrays, _ = oracle.parse_image(w.image)
+    assert (img.array("hi_out") == oracle.hist(arrays["hi_x"])).all()
+
+
+@pytest.mark.gpu
+def test_requires_violation_fails_loudly_on_device(gpu):
+    """A BatchNorm launch with HW % 4 != 0 is refused at bind time (InvalidArgument), not run
+    into wrong statistics; the same kernel launches once the precondition holds."""
+    hf = gpu
+    bad = hf.Image(pairs._bn(2, 3, 18)(0).image).upload()
+    mod = hf.Module.kernel(pairs.source("b200", "batchnorm"), grid=4)
+    with pytest.raises(hf.HFuseError) as e:
+        mod.run(bad, 4)
+    assert e.value.name == "InvalidArgument" and "bn_HW % 4 == 0" in str(e.value) and "bn_HW = 18" in str(e.value)
+    good = hf.Image(pairs._bn(2, 3, 16)(0).image).upload()
+    mod.run(good, 4)
