@@ -902,7 +902,10 @@ class Parser {
 
 }  // namespace
 
-Program parse_unchecked(const std::string& src, Dialect d) { return Parser(src, d).run(); }
+Program parse_unchecked(const std::string& src, Dialect d) {
+  if (d == Dialect::B200 && looks_like_cuda(src)) return Parser(cuda_to_mk(src), d).run();
+  return Parser(src, d).run();
+}
 
 Program parse(const std::string& src, Dialect d) {
   Program p = parse_unchecked(src, d);

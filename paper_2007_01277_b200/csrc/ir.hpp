@@ -203,7 +203,11 @@ bool has_calls(const Block& b);
 bool uses_extensions(const Kernel& k);
 
 // ---- frontend -----------------------------------------------------------------
-enum class Dialect { Strict, B200 };  // Strict = the reference grammar byte for byte
+enum class Dialect { Strict, B200 };
+// Restricted-CUDA input (cuda_frontend.cpp): a source with a `__global__` kernel is translated
+// to MK+ text (same line numbers) before parsing in the B200 dialect.
+bool looks_like_cuda(const std::string& src);
+std::string cuda_to_mk(const std::string& src);  // Strict = the reference grammar byte for byte
 Program parse_unchecked(const std::string& src, Dialect d = Dialect::B200);
 Program parse(const std::string& src, Dialect d = Dialect::B200);  // + validate()
 void validate(const Program& p);
