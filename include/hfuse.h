@@ -110,6 +110,8 @@ typedef struct hf_search_opts {
   int budget_points;        /* budget shares per partition (0: 5) */
   int best_regs1;           /* out: budgets of the best point (0 when it has none) */
   int best_regs2;           /* out */
+  int prefilter;            /* B200 model pre-filter: keep the k best-predicted partitions (0 off) */
+  char* model_csv;          /* out: "d1,predicted_us" per partition when the pre-filter ran (hf_free) */
 } hf_search_opts;
 
 typedef struct hf_device_props {

@@ -466,6 +466,7 @@ int hf_search(const char* src1, const char* src2, hf_image* img, hf_search_opts*
     so.granularity = o.granularity > 0 ? o.granularity : 128;
     for (int i = 0; i < o.n_extra_caps; ++i) so.extra_caps.push_back(o.extra_caps[i]);
     so.interval_regs = o.interval_regs != 0;
+    so.prefilter = o.prefilter;
     if (o.budget_points > 0) so.budget_points = o.budget_points;
     hf::SearchResult r = (n1.tunable && n2.tunable) ? hf::search_config(n1, n2, o.d0, *be, sm, so)
                                                     : hf::fixed_partition_fuse(n1, n2, *be, sm, o.d0, so);
@@ -476,6 +477,16 @@ int hf_search(const char* src1, const char* src2, hf_image* img, hf_search_opts*
     if (opts) {
       opts->best_regs1 = r.best_cfg.regs1;
       opts->best_regs2 = r.best_cfg.regs2;
+      opts->model_csv = nullptr;
+      if (!r.predicted_us.empty()) {
+        std::string m = "d1,predicted_us\n";
+        char buf[64];
+        for (const auto& [d1, t] : r.predicted_us) {
+          std::snprintf(buf, sizeof(buf), "%d,%.3f\n", d1, t);
+          m += buf;
+        }
+        opts->model_csv = dup(m);
+      }
     }
     if (trace) *trace = dup(hf::trace_csv(r));
     if (best_src) *best_src = dup(hf::emit(r.best, style_of(o.out_style)));

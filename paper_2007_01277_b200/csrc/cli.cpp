@@ -7,6 +7,7 @@
 //   hfuse search K1 K2 [--d0 N] --mem IMG... [--trace F] [-o F] [--style S] [--profiler-cmd CMD]
 //                      [--granularity G] [--caps 32,40,...] [--reps N] [--budgets]
 //                      (--budgets: also sweep per-interval setmaxnreg register budgets)
+//                      [--prefilter K]  (time only the K partitions the B200 model ranks best)
 //   hfuse occupancy [K] [--regs N --shmem B --threads T] [--sm S]
 //   hfuse check K              hfuse lower K [-o F]           hfuse emit K [-o F]
 //   hfuse profile CANDIDATE(.cu|.mk) --mem IMG... [--grid G]   (mkfuse --profiler-cmd target)
@@ -36,6 +37,7 @@ struct Args {
   std::optional<uint64_t> seed;
   std::string sm = "pascal-like", regcap = "auto", style, out, trace, entry, profiler_cmd, dump, caps, iregs;
   bool sequential = false, sm_given = false, regcap_given = false, budgets = false;
+  int prefilter = 0;
   int d0 = 1024, d1 = 0, d2 = 0, regs = 0, threads = 0, granularity = 128, reps = 10, warmup = 3, grid = 0;
   int64_t shmem = 0;
 };
@@ -89,6 +91,7 @@ Args parse_args(int argc, char** argv) {
     else if (s == "--granularity") a.granularity = num();
     else if (s == "--caps") a.caps = val();
     else if (s == "--interval-regs") a.iregs = val();
+    else if (s == "--prefilter") a.prefilter = num();
     else if (s == "--reps") a.reps = num();
     else if (s == "--warmup") a.warmup = num();
     else if (s == "--grid") a.grid = num();
@@ -200,6 +203,7 @@ int cmd_search(const Args& a) {
   SearchOptions so;
   so.granularity = a.granularity;
   so.interval_regs = a.budgets;
+  so.prefilter = a.prefilter;
   if (!a.caps.empty()) {
     std::stringstream ss(a.caps);
     std::string c;

@@ -35,6 +35,9 @@ class ProfilerBackend {
   virtual void prepare(const std::vector<std::pair<Fused, FusionConfig>>& candidates) { (void)candidates; }
   // Whether evaluate() honours per-interval register budgets (only sm100 code carries them).
   virtual bool supports_budgets() const { return false; }
+  // Calibration for the model pre-filter: the time of one constituent run alone with `threads`
+  // threads per block (partition_dims), or nullopt when the backend cannot measure it.
+  virtual std::optional<double> member_time(const Kernel& k, int threads) { return std::nullopt; }
 };
 
 // Spawns `command <source-file>` and reads the first integer of its stdout (search.cpp:32-62).
@@ -59,10 +62,12 @@ class DeviceBackend : public ProfilerBackend {
   Resources resources(const Kernel& k, int threads) override;
   void prepare(const std::vector<std::pair<Fused, FusionConfig>>& candidates) override;
   bool supports_budgets() const override { return true; }
+  std::optional<double> member_time(const Kernel& k, int threads) override;
   void set_specialization(std::map<std::string, ScalarVal> s) { spec_ = std::move(s); }
 
  private:
   std::map<std::string, ScalarVal> spec_;
+  std::map<std::pair<std::string, int>, double> member_us_;  // (emitted member source, threads)
   Image& img_;
   int grid_, warmup_, reps_;
   bool flush_, measured_;
@@ -80,6 +85,7 @@ struct SearchResult {
   FusionConfig best_cfg;
   int64_t best_time = 0;
   std::vector<EvalPoint> trace;
+  std::map<int, double> predicted_us;  // model pre-filter: d1 -> predicted time (all partitions)
 };
 
 struct SearchOptions {
@@ -90,6 +96,12 @@ struct SearchOptions {
   // shares of the constituents' register shortfall (interval_budgets()).
   bool interval_regs = false;
   int budget_points = 5;
+  // B200 model pre-filter: when > 0 and the backend can time constituents
+  // alone, each partition is predicted as max(t1(d1), t2(d2)) -- the two intervals run side by
+  // side, the slower one sets the time -- from the constituents measured alone at each
+  // interval size (one cheap compile + timing per (kernel, size), reused across partitions),
+  // and only the `prefilter` best-predicted partitions are fused, compiled and timed.
+  int prefilter = 0;
 };
 
 // Per-interval budgets for one partition: demand n1, n2 (ptxas registers of each constituent

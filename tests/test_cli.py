@@ -108,3 +108,12 @@ def test_search_sweeps_interval_budgets_with_profiler_command(tmp_path):
     assert budgets and all(row[3] == "5" for row in rows if "/" in row[2])
     assert "best_interval_regs = " + budgets[0] in r.stdout
     assert "setmaxnreg" in (tmp_path / "w.cu").read_text()
+
+
+def test_prefilter_needs_a_measuring_backend(corpus, tmp_path):
+    """The model pre-filter times constituents alone; a profiler command cannot, so the sweep
+    stays exhaustive (the reference's 14 points)."""
+    write_corpus(corpus, tmp_path)
+    r = run("search", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--profiler-cmd", "echo 11",
+            "--prefilter", 2)
+    assert r.returncode == 0 and "evaluated = 14" in r.stdout

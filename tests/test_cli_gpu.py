@@ -63,3 +63,22 @@ def test_search_on_device_and_profile_command(gpu, corpus, tmp_path):
     assert p.returncode == 0, p.stderr
     first = p.stdout.split()[0]
     assert first.isdigit() and int(first) > 0
+
+
+@pytest.mark.gpu
+def test_search_with_model_prefilter(gpu, corpus, tmp_path):
+    """`--prefilter 2`: the 7 partitions are ranked by the model (constituents timed alone), only
+    2 of them are fused and timed (uncapped + r0 each), every trace row carries its prediction."""
+    write_corpus(corpus, tmp_path)
+    trace = tmp_path / "t.csv"
+    r = run("search", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--mem", tmp_path / "batchnorm.img",
+            "--mem", tmp_path / "histogram.img", "--trace", trace, "--reps", 3, "--prefilter", 2)
+    assert r.returncode == 0, r.stderr
+    assert "evaluated = 4" in r.stdout
+    rows = trace.read_text().splitlines()
+    assert rows[0] == "d1,d2,reg_cap,cycles,occupancy,utilization,us,predicted_us" and len(rows) == 5
+    assert all(float(row.split(",")[-1]) > 0 for row in rows[1:])
+    hf = gpu
+    img = hf.Image(corpus["images"]["batchnorm"]).merge(hf.Image(corpus["images"]["histogram"])).upload()
+    res = hf.search(corpus["kernels"]["batchnorm"], corpus["kernels"]["histogram"], img, reps=3, prefilter=2)
+    assert sorted(res["model"]) == [128, 256, 384, 512, 640, 768, 896] and len(res["trace"]) == 4
