@@ -111,7 +111,9 @@ typedef struct hf_search_opts {
   int best_regs1;           /* out: budgets of the best point (0 when it has none) */
   int best_regs2;           /* out */
   int prefilter;            /* B200 model pre-filter: keep the k best-predicted partitions (0 off) */
-  char* model_csv;          /* out: "d1,predicted_us" per partition when the pre-filter ran (hf_free) */
+  double prefilter_tol;     /* ... and all predicted within this fraction of the best (< 0: 0.03) */
+  char* model_csv;          /* out: "d1,predicted_us,t1_us,t2_us" per partition (row d1 = 0: the
+                               full-block times) when the pre-filter ran; release with hf_free */
 } hf_search_opts;
 
 typedef struct hf_device_props {

@@ -467,6 +467,7 @@ int hf_search(const char* src1, const char* src2, hf_image* img, hf_search_opts*
     for (int i = 0; i < o.n_extra_caps; ++i) so.extra_caps.push_back(o.extra_caps[i]);
     so.interval_regs = o.interval_regs != 0;
     so.prefilter = o.prefilter;
+    if (o.prefilter_tol >= 0) so.prefilter_tol = o.prefilter_tol;
     if (o.budget_points > 0) so.budget_points = o.budget_points;
     hf::SearchResult r = (n1.tunable && n2.tunable) ? hf::search_config(n1, n2, o.d0, *be, sm, so)
                                                     : hf::fixed_partition_fuse(n1, n2, *be, sm, o.d0, so);
@@ -479,10 +480,13 @@ int hf_search(const char* src1, const char* src2, hf_image* img, hf_search_opts*
       opts->best_regs2 = r.best_cfg.regs2;
       opts->model_csv = nullptr;
       if (!r.predicted_us.empty()) {
-        std::string m = "d1,predicted_us\n";
-        char buf[64];
-        for (const auto& [d1, t] : r.predicted_us) {
-          std::snprintf(buf, sizeof(buf), "%d,%.3f\n", d1, t);
+        // d1,predicted,t1(d1),t2(d0-d1); the d1 = 0 row holds the full-block times T1, T2
+        std::string m = "d1,predicted_us,t1_us,t2_us\n";
+        char buf[128];
+        for (const auto& [d1, tt] : r.member_us) {
+          auto p = r.predicted_us.find(d1);
+          std::snprintf(buf, sizeof(buf), "%d,%.3f,%.3f,%.3f\n", d1, p == r.predicted_us.end() ? 0.0 : p->second,
+                        tt.first, tt.second);
           m += buf;
         }
         opts->model_csv = dup(m);

@@ -7,7 +7,8 @@
 //   hfuse search K1 K2 [--d0 N] --mem IMG... [--trace F] [-o F] [--style S] [--profiler-cmd CMD]
 //                      [--granularity G] [--caps 32,40,...] [--reps N] [--budgets]
 //                      (--budgets: also sweep per-interval setmaxnreg register budgets)
-//                      [--prefilter K]  (time only the K partitions the B200 model ranks best)
+//                      [--prefilter K [--prefilter-tol F]]  (time only the K partitions the B200
+//                      model ranks best, plus those predicted within F of the best; default 0.03)
 //   hfuse occupancy [K] [--regs N --shmem B --threads T] [--sm S]
 //   hfuse check K              hfuse lower K [-o F]           hfuse emit K [-o F]
 //   hfuse profile CANDIDATE(.cu|.mk) --mem IMG... [--grid G]   (mkfuse --profiler-cmd target)
@@ -38,6 +39,7 @@ struct Args {
   std::string sm = "pascal-like", regcap = "auto", style, out, trace, entry, profiler_cmd, dump, caps, iregs;
   bool sequential = false, sm_given = false, regcap_given = false, budgets = false;
   int prefilter = 0;
+  double prefilter_tol = -1.0;
   int d0 = 1024, d1 = 0, d2 = 0, regs = 0, threads = 0, granularity = 128, reps = 10, warmup = 3, grid = 0;
   int64_t shmem = 0;
 };
@@ -92,6 +94,7 @@ Args parse_args(int argc, char** argv) {
     else if (s == "--caps") a.caps = val();
     else if (s == "--interval-regs") a.iregs = val();
     else if (s == "--prefilter") a.prefilter = num();
+    else if (s == "--prefilter-tol") a.prefilter_tol = std::stod(val());
     else if (s == "--reps") a.reps = num();
     else if (s == "--warmup") a.warmup = num();
     else if (s == "--grid") a.grid = num();
@@ -204,6 +207,7 @@ int cmd_search(const Args& a) {
   so.granularity = a.granularity;
   so.interval_regs = a.budgets;
   so.prefilter = a.prefilter;
+  if (a.prefilter_tol >= 0) so.prefilter_tol = a.prefilter_tol;
   if (!a.caps.empty()) {
     std::stringstream ss(a.caps);
     std::string c;

@@ -95,7 +95,7 @@ class _SearchOpts(C.Structure):
                 ("specialize", C.c_int), ("n_extra_caps", C.c_int), ("extra_caps", C.POINTER(C.c_int)),
                 ("out_style", C.c_int), ("interval_regs", C.c_int), ("budget_points", C.c_int),
                 ("best_regs1", C.c_int), ("best_regs2", C.c_int), ("prefilter", C.c_int),
-                ("model_csv", C.c_void_p)]
+                ("prefilter_tol", C.c_double), ("model_csv", C.c_void_p)]
 
 
 class _Props(C.Structure):
@@ -532,19 +532,31 @@ def profile(src1: str, src2: str, d1: int, d2: int, img: Image, regcap="off", gr
             "regs": e.regs}
 
 
+def _model(p) -> dict:
+    """Pre-filter model rows: {"model": d1 -> predicted us, "member_us": d1 -> (t1, t2), with
+    d1 = 0 holding the full-block times (T1, T2)}."""
+    if not p:
+        return {"model": {}, "member_us": {}}
+    rows = [line.split(",") for line in _take(C.c_void_p(p)).strip().splitlines()[1:]]
+    return {"model": {int(r[0]): float(r[1]) for r in rows if int(r[0]) > 0},
+            "member_us": {int(r[0]): (float(r[2]), float(r[3])) for r in rows}}
+
+
 def search(src1: str, src2: str, img: Optional[Image] = None, d0: int = 1024, granularity: int = 128,
            profiler_cmd: Optional[str] = None, grid: int = 0, warmup: int = 3, reps: int = 10,
            flush_l2: bool = True, measured_registers: bool = True, extra_caps: Sequence[int] = (),
            out_style: str = "structured", specialize: bool = False, interval_regs: bool = False,
-           budget_points: int = 5, prefilter: int = 0) -> dict:
+           budget_points: int = 5, prefilter: int = 0, prefilter_tol: float = -1.0) -> dict:
     """interval_regs: also sweep per-interval register budgets (setmaxnreg) for warpgroup-
     aligned partitions; the best point's budgets come back as "interval_regs" (or None).
     prefilter: keep only the k partitions the B200 model predicts fastest (max of the two
-    constituents timed alone at each interval size); "model" maps d1 -> predicted us."""
+    constituents timed alone at each interval size) plus those predicted within prefilter_tol
+    (default 3 %) of the best; "model" maps d1 -> predicted us."""
     caps = (C.c_int * max(1, len(extra_caps)))(*extra_caps)
     o = _SearchOpts(d0, granularity, 1 if profiler_cmd else 0, _b(profiler_cmd), grid, warmup, reps,
                     int(flush_l2), int(measured_registers), int(specialize), len(extra_caps), caps,
-                    STYLES[out_style], int(interval_regs), budget_points, 0, 0, prefilter, None)
+                    STYLES[out_style], int(interval_regs), budget_points, 0, 0, prefilter, prefilter_tol,
+                    None)
     d1, d2, cap, best = C.c_int(), C.c_int(), C.c_int(), C.c_longlong()
     trace, src, err = C.c_void_p(), C.c_void_p(), _Err()
     _check(_lib.hf_search(src1.encode(), src2.encode(), img._h if img else None, C.byref(o), C.byref(d1),
@@ -559,6 +571,5 @@ def search(src1: str, src2: str, img: Optional[Image] = None, d0: int = 1024, gr
         rows.append({k: (v if k == "reg_cap" else float(v) if "." in v else int(v)) for k, v in zip(keys, vals)})
     return {"d1": d1.value, "d2": d2.value, "reg_cap": None if cap.value < 0 else cap.value,
             "interval_regs": (o.best_regs1, o.best_regs2) if o.best_regs1 > 0 else None,
-            "model": {int(line.split(",")[0]): float(line.split(",")[1])
-                      for line in _take(C.c_void_p(o.model_csv)).strip().splitlines()[1:]} if o.model_csv else {},
+            **_model(o.model_csv),
             "best_time": best.value, "trace_csv": csv, "trace": rows, "source": _take(src)}

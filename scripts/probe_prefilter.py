@@ -31,6 +31,7 @@ for a, b in P.PAIRS:
     for row in ex["trace"]:
         measured[row["d1"]] = min(measured.get(row["d1"], 1e30), row["us"])
     model = pf["model"]
+    mem = pf["member_us"]
     common = sorted(set(measured) & set(model))
     rank_m = sorted(common, key=lambda d: measured[d])
     rank_p = sorted(common, key=lambda d: model[d])
@@ -43,6 +44,7 @@ for a, b in P.PAIRS:
         "best_measured_rank_in_model": rank_p.index(rank_m[0]) + 1 if common else None,
         "model_us": {str(d): round(model[d], 2) for d in common},
         "measured_us": {str(d): round(measured[d], 2) for d in common},
+        "member_us": {str(d): [round(x, 2) for x in v] for d, v in mem.items()},
     }
     print(a, b, json.dumps({k: v for k, v in out["pairs"][f"{a}+{b}"].items() if k in ("exhaustive", "prefilter", "ratio", "best_measured_rank_in_model")}), flush=True)
 r = [p["ratio"] for p in out["pairs"].values()]

@@ -72,7 +72,8 @@ def test_search_with_model_prefilter(gpu, corpus, tmp_path):
     write_corpus(corpus, tmp_path)
     trace = tmp_path / "t.csv"
     r = run("search", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--mem", tmp_path / "batchnorm.img",
-            "--mem", tmp_path / "histogram.img", "--trace", trace, "--reps", 3, "--prefilter", 2)
+            "--mem", tmp_path / "histogram.img", "--trace", trace, "--reps", 3, "--prefilter", 2,
+            "--prefilter-tol", 0)
     assert r.returncode == 0, r.stderr
     assert "evaluated = 4" in r.stdout
     rows = trace.read_text().splitlines()
@@ -80,5 +81,6 @@ def test_search_with_model_prefilter(gpu, corpus, tmp_path):
     assert all(float(row.split(",")[-1]) > 0 for row in rows[1:])
     hf = gpu
     img = hf.Image(corpus["images"]["batchnorm"]).merge(hf.Image(corpus["images"]["histogram"])).upload()
-    res = hf.search(corpus["kernels"]["batchnorm"], corpus["kernels"]["histogram"], img, reps=3, prefilter=2)
+    res = hf.search(corpus["kernels"]["batchnorm"], corpus["kernels"]["histogram"], img, reps=3, prefilter=2,
+                    prefilter_tol=0.0)
     assert sorted(res["model"]) == [128, 256, 384, 512, 640, 768, 896] and len(res["trace"]) == 4
