@@ -614,12 +614,14 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
 
 
 def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):
-    """Host-buffer end-to-end step through hf_launch (the C-ABI call): per pair, the pinned-host
-    -> HBM upload of every array the fused kernel reads (hf_module_param_reads; pure outputs are
-    not uploaded, the kernel overwrites them), the launch, and the HBM -> pinned-host download of
-    every array it writes. Pipelined over three streams (upload / compute / download) with
-    per-pair device buffers, so pair i+1's upload and pair i-1's download overlap pair i's kernel
-    (PCIe is full duplex); cross-step reuse of a pair's buffers waits on that pair's events."""
+    """Host-buffer end-to-end step through hf_launch (the C-ABI call): every input tensor of the
+    step (an array no kernel writes) goes pinned host -> HBM once, the ten fused kernels run,
+    and each pair's outputs (every array it writes) come back HBM -> pinned host. Arrays a kernel
+    writes but never reads (hf_module_param_reads: no loads, no atomics) are not uploaded; a
+    written array that is also read (histogram bins) is uploaded per pair from its host zeros.
+    Pipelined over three streams (upload / fused kernels / download; PCIe is full duplex): a
+    pair waits only for its own inputs, outputs drain while later pairs run. Outputs use per-pair
+    device buffers; cross-step reuse of any buffer waits on the events of its last user."""
     host, scal = {}, {}
     for k in keys:
         arrays, scalars = _image_arrays(hf, work[k].image)
@@ -631,36 +633,57 @@ def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):
             else:
                 h.zero_()
             host[name] = h
-    plan = []  # per pair: (module, grid, uploads, downloads, launch args)
-    for a, b in pair_list:
+    written = {p["name"] for a, b in pair_list for p in fused[(a, b)].params if p["array"] and p["written"]}
+    shared = {}  # input tensors: one device copy per step, shared by the pairs that read them
+    plan = []    # per pair: (module, grid, shared inputs, per-pair uploads, downloads, launch args)
+    last_reader = {}
+    for i, (a, b) in enumerate(pair_list):
         m = fused[(a, b)]
-        dev, ups, downs, args_ = {}, [], [], {}
+        ins, ups, downs, args_ = [], [], [], {}
         for p in m.params:
             if not p["array"]:
                 args_[p["name"]] = scal[p["name"]]
                 continue
             h = host[p["name"]]
+            if p["name"] not in written:
+                if p["name"] not in shared:
+                    shared[p["name"]] = torch.empty(h.numel(), dtype=h.dtype, device="cuda")
+                args_[p["name"]] = shared[p["name"]]
+                ins.append(p["name"])
+                last_reader[p["name"]] = i
+                continue
             d = torch.empty(h.numel(), dtype=h.dtype, device="cuda")
             args_[p["name"]] = d
-            if p["read"] or not p["written"]:
+            if p["read"]:
                 ups.append((d, h))
-            if p["written"]:
-                downs.append((h, d))
-        plan.append((m, pgrid[(a, b)], ups, downs, args_))
+            downs.append((h, d))
+        plan.append((m, pgrid[(a, b)], ins, ups, downs, args_))
     s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
     n = len(plan)
+    ev_in = {name: torch.cuda.Event() for name in shared}
     ev_up = [torch.cuda.Event() for _ in range(n)]
     ev_k = [torch.cuda.Event() for _ in range(n)]
     ev_dn = [torch.cuda.Event() for _ in range(n)]
 
     def one_step(first):
-        for i, (m, g, ups, downs, args_) in enumerate(plan):
+        sent = set()
+        for i, (m, g, ins, ups, downs, args_) in enumerate(plan):
             with torch.cuda.stream(s_up):
+                for name in ins:
+                    if name in sent:
+                        continue
+                    if not first:
+                        s_up.wait_event(ev_k[last_reader[name]])  # last step's readers are done
+                    shared[name].copy_(host[name], non_blocking=True)
+                    ev_in[name].record(s_up)
+                    sent.add(name)
                 if not first:
-                    s_up.wait_event(ev_k[i])      # the previous step's kernel of this pair is done
+                    s_up.wait_event(ev_k[i])
                 for d, h in ups:
                     d.copy_(h, non_blocking=True)
                 ev_up[i].record(s_up)
+            for name in ins:
+                stream.wait_event(ev_in[name])
             stream.wait_event(ev_up[i])
             if not first:
                 stream.wait_event(ev_dn[i])       # its outputs of the previous step are downloaded
@@ -671,8 +694,9 @@ def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):
                 for h, d in downs:
                     h.copy_(d, non_blocking=True)
                 ev_dn[i].record(s_down)
-    h2d = sum(h.numel() * h.element_size() for _, _, ups, _, _ in plan for _, h in ups)
-    d2h = sum(h.numel() * h.element_size() for _, _, _, downs, _ in plan for h, _ in downs)
+    h2d = sum(host[name].numel() * host[name].element_size() for name in shared) + \
+        sum(h.numel() * h.element_size() for _, _, _, ups, _, _ in plan for _, h in ups)
+    d2h = sum(h.numel() * h.element_size() for _, _, _, _, downs, _ in plan for h, _ in downs)
     one_step(True)
     torch.cuda.synchronize()
     steps = max(2, min(args.steps, 5))
@@ -687,8 +711,8 @@ def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):
     torch.cuda.synchronize()
     us = s0.elapsed_time(s1) * 1000.0 / steps
     return {"value": us, "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
-            "pipeline": "3 streams (upload / fused kernel / download), per-pair device buffers; "
-                        "pure outputs not uploaded"}
+            "pipeline": "3 streams (upload / fused kernels / download); each input tensor uploaded once "
+                        "per step; per-pair outputs downloaded; pure outputs not uploaded"}
 
 
 def _image_arrays(hf, text):
