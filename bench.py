@@ -127,6 +127,40 @@ def cpu_baseline(pairs_mod, steps=1):
                 "sample": f"C restatement on 1/{SAMPLE_DIV} of every member x 4 pair-appearances"}
 
 
+_COLL = {}
+
+
+def _install_collectives(dist, backend):
+    """all_reduce / all_gather on CUDA tensors: NCCL directly; other backends (the one-GPU
+    gloo validation of the multi-rank path) stage through host memory."""
+    _COLL["dist"], _COLL["backend"] = dist, backend
+
+
+def all_reduce(t, op="sum"):
+    dist = _COLL["dist"]
+    o = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}[op]
+    if _COLL["backend"] == "nccl":
+        dist.all_reduce(t, op=o)
+        return t
+    c = t.cpu()
+    dist.all_reduce(c, op=o)
+    t.copy_(c)
+    return t
+
+
+def all_gather(t, world):
+    import torch
+    dist = _COLL["dist"]
+    if _COLL["backend"] == "nccl":
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return parts
+    c = t.cpu()
+    parts = [torch.empty_like(c) for _ in range(world)]
+    dist.all_gather(parts, c)
+    return [p.to(t.device) for p in parts]
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -142,7 +176,10 @@ def run_reference_arm(args):
             cpu_reference_step(pairs_mod, d, cores)
         walls = [cpu_reference_step(pairs_mod, d, cores) for _ in range(args.steps)]
     wall = statistics.median(walls)
-    us = wall * SAMPLE_DIV * 1e6
+    # weak scaling: the N-GPU job is N batch shards of this workload; the CPU reference runs
+    # them one after another on the same cores (one shard measured, N times its time)
+    shards = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    us = wall * SAMPLE_DIV * 1e6 * shards
     line = {
         "metric": METRIC, "impl": "reference", "value": us, "unit": "us", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
@@ -151,7 +188,8 @@ def run_reference_arm(args):
                                f"sequential run_functional, extrapolated from a 1/{SAMPLE_DIV} sample",
                    "sample_div": SAMPLE_DIV},
         "cpu_baseline": {"value": us, "unit": "us", "cores": cores, "kind": "reference",
-                         "sample": f"mkfuse_ref seq on 1/{SAMPLE_DIV} of each member, 10 pairs over {cores} processes"},
+                         "sample": f"mkfuse_ref seq on 1/{SAMPLE_DIV} of each member, 10 pairs over {cores} processes"
+                                   + (f", x {shards} shards (weak scaling)" if shards > 1 else "")},
         "e2e": {"value": us, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -247,11 +285,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HF_BENCH_DIST=gloo: the multi-rank path validated on ONE GPU (ranks share cuda:0, the
+    # collectives go through host memory); production runs use NCCL, one rank per GPU
+    backend = os.environ.get("HF_BENCH_DIST", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    _install_collectives(dist, backend)
     from paper_2007_01277_b200 import hfuse as hf
     from paper_2007_01277_b200 import pairs as P
 
@@ -334,11 +381,11 @@ def main():
         if "hist" in keys:
             bins = torch.empty(64, dtype=torch.int32, device="cuda")
             cudart_copy(bins, img.device_ptr("hi_out"), 64 * 4)
-            dist.all_reduce(bins)
+            all_reduce(bins)
         if "bn" in keys:
             st = torch.empty(512, dtype=torch.float32, device="cuda")
             cudart_copy(st, img.device_ptr("bn_stats"), 512 * 4)
-            dist.all_gather([torch.empty_like(st) for _ in range(world)], st)
+            all_gather(st, world)
 
     # ---- timed region: K steps of the ten fused kernels, back to back on one stream
     def step(record=None):
@@ -390,7 +437,7 @@ def main():
     total_ms = t0.elapsed_time(t1)
     ms = torch.tensor([total_ms, u0.elapsed_time(u1)], device="cuda")
     if dist is not None:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        all_reduce(ms, "max")
     us_per_step = ms[0].item() * 1000.0 / args.steps
     unfused_us_per_step = ms[1].item() * 1000.0 / args.steps
 
@@ -574,8 +621,8 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
         if world > 1:
             import torch.distributed as dist
             hits, win = hits.cuda(), win.cuda()
-            dist.all_reduce(hits)
-            dist.all_reduce(win, op=dist.ReduceOp.MIN)
+            all_reduce(hits)
+            all_reduce(win, "min")
         res["hits"] = hits.tolist()
         res["winning_nonce"] = win.tolist()
         out["c3"].append(res)
