@@ -1,0 +1,51 @@
+"""Small launches of every fused-kernel family for compute-sanitizer (memcheck / racecheck /
+synccheck): named-barrier rewriting must not introduce shared-memory races or barrier misuse.
+  compute-sanitizer --tool racecheck python scripts/sanitize_targets.py
+Covers: corpus pairs (reference Mini-Kernel), the ten DL pairs (B200 forms, parity sizes, two
+splits), the crypto pairs (one register cap and per-interval budgets), the hand-off BatchNorm,
+and a CUDA-frontend pair."""
+import os
+import sys
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from conftest import golden  # noqa: E402
+from paper_2007_01277_b200 import crypto as CR  # noqa: E402
+from paper_2007_01277_b200 import hfuse as hf  # noqa: E402
+from paper_2007_01277_b200 import pairs as P  # noqa: E402
+
+n = 0
+corpus = golden("corpus_sources.json")
+for a, b in [("histogram", "batchnorm"), ("batchnorm", "shuffle_reduce"), ("streamer", "hasher"),
+             ("strided_sum", "histogram")]:
+    m = hf.Module.fused(corpus["kernels"][a], corpus["kernels"][b], 512, 512)
+    img = hf.Image(corpus["images"][a]).merge(hf.Image(corpus["images"][b])).upload()
+    m.run(img)
+    n += 1
+for a, b in P.PAIRS:
+    img = hf.Image(P.MEMBERS[a].sizes["parity"](0).image).merge(hf.Image(P.MEMBERS[b].sizes["parity"](0).image)).upload()
+    for d1 in (256, 768):
+        hf.Module.fused(P.source("b200", P.MEMBERS[a].stem), P.source("b200", P.MEMBERS[b].stem), d1, 1024 - d1,
+                        grid=4).run(img, 4)
+        n += 1
+src = {k: open(os.path.join(P.KERNELS, "b200", k + ".mk")).read() for k in CR.MEMBERS}
+for a, b, d2, regs in [("sha256d", "blake2b", 512, (40, 56)), ("blake256", "ethash", 384, (32, 120))]:
+    wa = CR.workload(a, 1024, 2, nonce0=5, target=1 << 28)
+    wb = CR.workload(b, 256 if b == "ethash" else 1024, 2, nonce0=9, target=1 << 28)
+    img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
+    hf.Module.fused(src[a], src[b], 512, d2, grid=2, specialize=img).run(img, 2)
+    hf.Module.fused_regs(src[a], src[b], 512, d2, *regs, grid=2, specialize=img).run(img, 2)
+    n += 2
+img = hf.Image(P._bn(2, 8, 56 * 56, slots=256)(0).image).upload()
+hf.Module.kernel(P.source("b200", "batchnorm_warp"), grid=7).run(img, 7)
+n += 1
+cu = os.path.join(ROOT, "tests", "cuda")
+m = hf.Module.fused(open(os.path.join(cu, "histogram.cu")).read(), open(os.path.join(cu, "batchnorm.cu")).read(),
+                    128, 896)
+img = hf.Image(corpus["images"]["histogram"]).merge(hf.Image(corpus["images"]["batchnorm"])).upload()
+m.run(img)
+n += 1
+import ctypes  # noqa: E402
+assert ctypes.CDLL("libcudart.so.12").cudaDeviceSynchronize() == 0
+print(f"sanitize targets: {n} fused launches")
