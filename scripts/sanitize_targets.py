@@ -17,9 +17,11 @@ from paper_2007_01277_b200 import pairs as P  # noqa: E402
 
 n = 0
 corpus = golden("corpus_sources.json")
+digests = golden("corpus_digests.json")
 for a, b in [("histogram", "batchnorm"), ("batchnorm", "shuffle_reduce"), ("streamer", "hasher"),
              ("strided_sum", "histogram")]:
-    m = hf.Module.fused(corpus["kernels"][a], corpus["kernels"][b], 512, 512)
+    rec = digests["pairs"][f"{a}+{b}"]  # the acceptance splits: the corpus kernels are sized for them
+    m = hf.Module.fused(corpus["kernels"][a], corpus["kernels"][b], rec["d1"], rec["d2"])
     img = hf.Image(corpus["images"][a]).merge(hf.Image(corpus["images"][b])).upload()
     m.run(img)
     n += 1
