@@ -9,9 +9,14 @@
 //             block shape from `//@ block=X[,Y[,Z]]` or __launch_bounds__(N) -> (N, 1, 1);
 //             `//@ fixed` marks a non-tunable kernel; other `//@ key=value` items pass through
 //   functions `__device__ [__forceinline__|inline|static] int|float|void name(params) { ... }`
-//   params    `[const] int|float [*] [const] [__restrict__] name` (pointer = array)
+//   types     int, float, unsigned int / uint32_t (same 32-bit words; unsigned >>, <, /2^k, %2^k,
+//             min/max lower to shr_u / ltu / masks), float2/float4/int2/int4/uint2/uint4 locals
+//             (one scalar per component; v.x .. v.w), no 64-bit types
+//   params    `[const] T [*] [const] [__restrict__] name` (pointer = array)
 //   stmts     declarations (several declarators, initializers), `__shared__ T s[N]` (N a constant
 //             expression), `=` and compound assignments, `++`/`--`, if/else, for, while, return,
+//             vector loads/stores `reinterpret_cast<const float4*>(p)[i]` / `((float4*)p)[i]`
+//             (MK+ vload/vstore), `make_float4(..)`, `__ldg(&a[i])`,
 //             `{ }` blocks, `__syncthreads()`, `__syncwarp()`, `__threadfence()`,
 //             `atomicAdd(&a[i], v)` as a statement, device-function calls, `#pragma unroll [N]`
 //   exprs     C operators except ?:, assignment and comma; casts (int)/(float) and int()/float();
@@ -19,6 +24,8 @@
 //             gridDim, `__shfl_xor_sync(0xffffffff, v, m)`; float literals drop their f suffix
 // Semantics are the interpreter's: identical to CUDA for programs without
 // signed overflow / out-of-range shifts, except that floating-point contraction is never applied.
+// The builtins (threadIdx.x, ...) are typed int: CUDA's unsigned builtins give the same results
+// while indices stay below 2^31.
 // `x op= e` is `x = x op (e)`, as in C. Output keeps the CUDA line numbers (one output line per
 // input line) so later diagnostics point at the CUDA source.
 #include <cctype>
@@ -124,14 +131,20 @@ std::vector<CTok> ctokens(const std::string& s) {
           while (i < s.size() && std::isdigit(static_cast<unsigned char>(s[i]))) w.push_back(adv());
         }
       }
+      bool uns = false;
       while (i < s.size() && std::strchr("fFuUlL", s[i])) {
         char suf = adv();
         if (suf == 'f' || suf == 'F') {
           if (hex) raise(Code::Syntax, "malformed number", p);
           flt = true;
           if (w.find_first_of(".eE") == std::string::npos) w += ".0";
+        } else if (suf == 'u' || suf == 'U') {
+          uns = true;
+        } else {
+          raise(Code::Syntax, "CUDA: 64-bit literals are outside the CUDA subset", p);
         }
       }
+      if (uns && !flt) w += "u";  // unsigned int literal (the translator types it)
       out.push_back(CTok{flt ? CTok::Flt : CTok::Int, w, p});
       continue;
     }
@@ -158,10 +171,23 @@ std::vector<CTok> ctokens(const std::string& s) {
   return out;
 }
 
-// A translated expression (MK+ text).
+// A translated expression: MK+ text and its C type ('i' int, 'u' unsigned int, 'f' float).
 struct CE {
   std::string t;
+  char ty = 'i';
 };
+
+// A parsed C type: scalar base plus vector width (1, 2, 4).
+struct CT {
+  char base = 'i';
+  int width = 1;
+};
+
+const char* mk_type(char b) { return b == 'f' ? "float" : "int"; }
+const char* comp_name(int k) {
+  static const char* n[] = {"x", "y", "z", "w"};
+  return n[k];
+}
 
 class Translator {
  public:
@@ -204,7 +230,10 @@ class Translator {
   size_t at_ = 0;
   std::string out_;
   int out_line_ = 1;
-  int label_ = 0;
+  // symbols of the function being translated (C scoping is flattened: one type per name)
+  std::map<std::string, char> vars_, arrs_;
+  std::map<std::string, CT> vecs_;
+  std::map<std::string, char> funcs_;  // device function -> return type
 
   [[noreturn]] static void fail(const std::string& m, Pos p) { raise(Code::Syntax, "CUDA: " + m, p); }
   const CTok& peek(size_t o = 0) const { return toks_[std::min(at_ + o, toks_.size() - 1)]; }
@@ -231,27 +260,47 @@ class Translator {
     out_ += text;
   }
 
+  static bool is_qualifier(const std::string& w) {
+    return w == "const" || w == "__restrict__" || w == "restrict" || w == "volatile" || w == "__restrict" ||
+           w == "register";
+  }
   void skip_qualifiers() {
-    while (is_id("const") || is_id("__restrict__") || is_id("restrict") || is_id("volatile") ||
-           is_id("__restrict") || is_id("register"))
-      next();
+    while (peek().k == CTok::Id && is_qualifier(peek().t)) next();
   }
 
-  // int | float (unsigned, double, ... are outside the subset)
-  std::string type_name() {
+  static std::optional<CT> type_word(const std::string& w) {
+    static const std::map<std::string, CT> m = {
+        {"int", {'i', 1}},     {"float", {'f', 1}},   {"uint32_t", {'u', 1}}, {"int32_t", {'i', 1}},
+        {"float2", {'f', 2}},  {"float4", {'f', 4}},  {"int2", {'i', 2}},     {"int4", {'i', 4}},
+        {"uint2", {'u', 2}},   {"uint4", {'u', 4}},   {"unsigned", {'u', 1}}, {"signed", {'i', 1}}};
+    auto it = m.find(w);
+    if (it == m.end()) return std::nullopt;
+    return it->second;
+  }
+
+  CT type_name() {
     skip_qualifiers();
     const CTok& t = peek();
-    if (is_id("int") || is_id("float")) return next().t;
-    if (t.k == CTok::Id && (t.t == "unsigned" || t.t == "double" || t.t == "long" || t.t == "short" ||
-                            t.t == "char" || t.t == "bool" || t.t == "size_t" || t.t == "uint32_t"))
-      fail("type '" + t.t + "' is outside the CUDA subset (int and float only)", t.pos);
-    fail("expected a type (int or float), found '" + t.t + "'", t.pos);
+    if (t.k == CTok::Id) {
+      if (auto ct = type_word(t.t)) {
+        next();
+        if ((t.t == "unsigned" || t.t == "signed") && is_id("int")) next();
+        skip_qualifiers();
+        return *ct;
+      }
+      if (t.t == "double" || t.t == "long" || t.t == "short" || t.t == "char" || t.t == "bool" ||
+          t.t == "size_t" || t.t == "uint64_t" || t.t == "int64_t" || t.t == "half" || t.t == "__half")
+        fail("type '" + t.t + "' is outside the CUDA subset (32-bit int, unsigned, float and their 2/4-vectors)",
+             t.pos);
+    }
+    fail("expected a type, found '" + t.t + "'", t.pos);
   }
   bool at_type() const {
     size_t o = 0;
-    while (peek(o).k == CTok::Id && (peek(o).t == "const" || peek(o).t == "volatile" || peek(o).t == "register")) ++o;
-    return peek(o).k == CTok::Id && (peek(o).t == "int" || peek(o).t == "float" || peek(o).t == "unsigned" ||
-                                     peek(o).t == "double");
+    while (peek(o).k == CTok::Id && is_qualifier(peek(o).t)) ++o;
+    const CTok& t = peek(o);
+    return t.k == CTok::Id && (type_word(t.t) || t.t == "double" || t.t == "long" || t.t == "short" ||
+                               t.t == "char" || t.t == "bool" || t.t == "size_t" || t.t == "uint64_t");
   }
 
   std::string params() {
@@ -259,7 +308,8 @@ class Translator {
     std::string o;
     if (is_id("void") && is_op(")", 1)) next();
     while (!is_op(")")) {
-      std::string ty = type_name();
+      Pos tp = peek().pos;
+      CT ty = type_name();
       bool ptr = false;
       while (is_op("*")) {
         if (ptr) fail("pointer-to-pointer parameters are outside the subset", peek().pos);
@@ -273,7 +323,10 @@ class Translator {
         want_op("]");
         ptr = true;
       }
-      o += (o.empty() ? "" : ", ") + ty + " " + n.t + (ptr ? "[]" : "");
+      if (ty.width > 1) fail("vector-typed parameters are outside the subset (pass a scalar pointer)", tp);
+      if (ptr) arrs_[n.t] = ty.base;
+      else vars_[n.t] = ty.base;
+      o += (o.empty() ? "" : ", ") + std::string(mk_type(ty.base)) + " " + n.t + (ptr ? "[]" : "");
       if (is_op(",")) next();
       else if (!is_op(")")) fail("expected ',' or ')' in the parameter list", peek().pos);
     }
@@ -281,7 +334,14 @@ class Translator {
     return "(" + o + ")";
   }
 
+  void reset_symbols() {
+    vars_.clear();
+    arrs_.clear();
+    vecs_.clear();
+  }
+
   void kernel(const std::vector<CTok>& anns) {
+    reset_symbols();
     Pos p = next().pos;  // __global__
     skip_qualifiers();
     if (!is_id("void")) fail("a __global__ kernel must return void", peek().pos);
@@ -304,7 +364,6 @@ class Translator {
     std::string ps = params();
     int bx = 0, by = 1, bz = 1;
     bool fixed = false;
-    std::string pass;
     for (const auto& a : anns) {
       std::istringstream in(a.t);
       std::string item, rest;
@@ -341,14 +400,24 @@ class Translator {
   }
 
   void function() {
+    reset_symbols();
     while (is_id("__device__") || is_id("static") || is_id("inline") || is_id("__forceinline__") ||
            is_id("__noinline__"))
       next();
     std::string ret;
-    if (is_id("void")) ret = next().t;
-    else ret = type_name();
+    char rt = 'i';
+    if (is_id("void")) {
+      ret = next().t;
+    } else {
+      Pos tp = peek().pos;
+      CT t = type_name();
+      if (t.width > 1) fail("vector return types are outside the subset", tp);
+      rt = t.base;
+      ret = mk_type(t.base);
+    }
     if (is_op("*")) fail("pointer return types are outside the subset", peek().pos);
     CTok name = want_id();
+    funcs_[name.t] = rt;
     std::string ps = params();
     put(ret + " " + name.t + ps + " {", name.pos);
     block_body();
@@ -396,7 +465,9 @@ class Translator {
     }
     if (is_id("__shared__")) {
       next();
-      std::string ty = type_name();
+      Pos tp = peek().pos;
+      CT ty = type_name();
+      if (ty.width > 1) fail("vector-typed __shared__ arrays are outside the subset", tp);
       CTok n = want_id();
       want_op("[");
       CE len = expr();
@@ -405,7 +476,8 @@ class Translator {
       want_op("]");
       if (is_op("=")) fail("__shared__ arrays take no initializer", peek().pos);
       want_op(";");
-      put("shared " + ty + " " + n.t + "[" + std::to_string(*v) + "];", p);
+      arrs_[n.t] = ty.base;
+      put(std::string("shared ") + mk_type(ty.base) + " " + n.t + "[" + std::to_string(*v) + "];", p);
       return;
     }
     if (is_id("extern") && is_id("__shared__", 1)) fail("dynamic shared memory is outside the subset", p);
@@ -470,13 +542,31 @@ class Translator {
       next();
       want_op("(");
       want_op("&");
-      std::string lv = lvalue();
+      auto [lv, lt] = lvalue();
       want_op(",");
       CE v = expr();
       want_op(")");
       if (!is_op(";")) fail("the result of atomicAdd cannot be used in the CUDA subset", peek().pos);
       next();
-      put("atomic_add(" + lv + ", " + v.t + ");", p);
+      put("atomic_add(" + lv + ", " + conv(v, lt, p).t + ");", p);
+      return;
+    }
+    if (at_vector_ref()) {  // vector store
+      Pos sp = peek().pos;
+      auto [arr, idx, vt] = vector_ref();
+      want_op("=");
+      std::vector<std::string> vals = vector_value(vt, sp);
+      want_op(";");
+      std::string o = "vstore(" + arr + ", " + idx;
+      for (const auto& v : vals) o += ", " + v;
+      put(o + ");", p);
+      return;
+    }
+    if (peek().k == CTok::Id && vecs_.count(peek().t) && is_op("=", 1)) {  // vector assignment
+      CTok n = next();
+      next();
+      put(vector_assign(n.t, vecs_[n.t], n.pos), p);
+      want_op(";");
       return;
     }
     std::string s = simple();
@@ -487,18 +577,31 @@ class Translator {
   // Declaration statement (possibly several declarators) ending at `term`.
   void declaration(const char* term) {
     Pos p = peek().pos;
-    std::string ty = type_name();
+    CT ty = type_name();
     std::string o;
     while (true) {
       if (is_op("*")) fail("local pointers are outside the CUDA subset", peek().pos);
       CTok n = want_id();
       if (is_op("[")) fail("local arrays are outside the CUDA subset (Mini-Kernel has none)", peek().pos);
-      std::string d = ty + " " + n.t;
-      if (is_op("=")) {
-        next();
-        d += " = " + expr().t;
+      if (ty.width > 1) {
+        vecs_[n.t] = ty;  // the latest declaration of a name wins (C scopes flattened)
+        vars_.erase(n.t);
+        for (int k = 0; k < ty.width; ++k)
+          o += (o.empty() ? "" : " ") + std::string(mk_type(ty.base)) + " " + n.t + "_" + comp_name(k) + ";";
+        if (is_op("=")) {
+          next();
+          o += " " + vector_assign(n.t, ty, n.pos);
+        }
+      } else {
+        vars_[n.t] = ty.base;
+        vecs_.erase(n.t);
+        std::string d = std::string(mk_type(ty.base)) + " " + n.t;
+        if (is_op("=")) {
+          next();
+          d += " = " + conv(expr(), ty.base, n.pos).t;
+        }
+        o += (o.empty() ? "" : " ") + d + ";";
       }
-      o += (o.empty() ? "" : " ") + d + ";";
       if (is_op(",")) {
         next();
         continue;
@@ -509,15 +612,109 @@ class Translator {
     put(o, p);
   }
 
+  // ---- vectors ---------------------------------------------------------------------------
+  // reinterpret_cast<[const] T*>(p)[i]  or  ((const T*)p)[i]  with T a 2/4-vector type
+  bool at_vector_ref() const {
+    if (is_id("reinterpret_cast") && is_op("<", 1)) return true;
+    if (is_op("(") && is_op("(", 1)) {
+      size_t o = 2;
+      while (peek(o).k == CTok::Id && is_qualifier(peek(o).t)) ++o;
+      auto t = peek(o).k == CTok::Id ? type_word(peek(o).t) : std::nullopt;
+      return t && t->width > 1 && is_op("*", o + 1);
+    }
+    return false;
+  }
+
+  struct VRef {
+    std::string arr, idx;
+    CT ty;
+  };
+  VRef vector_ref() {
+    Pos p = peek().pos;
+    CT ty;
+    std::string arr;
+    if (is_id("reinterpret_cast")) {
+      next();
+      want_op("<");
+      ty = type_name();
+      want_op("*");
+      skip_qualifiers();
+      want_op(">");
+      want_op("(");
+      arr = want_id().t;
+      want_op(")");
+    } else {
+      want_op("(");
+      want_op("(");
+      ty = type_name();
+      want_op("*");
+      want_op(")");
+      arr = want_id().t;
+      want_op(")");
+    }
+    if (ty.width == 1) fail("only 2- and 4-wide vector casts are supported", p);
+    auto it = arrs_.find(arr);
+    if (it == arrs_.end()) fail("'" + arr + "' is not a pointer parameter or shared array", p);
+    if ((it->second == 'f') != (ty.base == 'f')) fail("vector cast changes the element type of '" + arr + "'", p);
+    want_op("[");
+    CE i = expr();
+    want_op("]");
+    return VRef{arr, conv(i, 'i', p).t, ty};
+  }
+
+  // the components of a vector-valued expression: make_T(..), a vector variable
+  std::vector<std::string> vector_value(CT ty, Pos p) {
+    std::vector<std::string> v;
+    if (peek().k == CTok::Id && peek().t.rfind("make_", 0) == 0) {
+      CTok f = next();
+      auto mt = type_word(f.t.substr(5));
+      if (!mt || mt->width != ty.width) fail("'" + f.t + "' does not build this vector type", f.pos);
+      std::vector<CE> a = call_args();
+      if (int(a.size()) != ty.width) fail(f.t + " takes " + std::to_string(ty.width) + " arguments", f.pos);
+      for (auto& e : a) v.push_back(conv(e, ty.base, f.pos).t);
+      return v;
+    }
+    if (peek().k == CTok::Id && vecs_.count(peek().t)) {
+      CTok n = next();
+      CT src = vecs_[n.t];
+      if (src.width != ty.width || (src.base == 'f') != (ty.base == 'f')) fail("vector type mismatch", n.pos);
+      for (int k = 0; k < ty.width; ++k) v.push_back(n.t + "_" + comp_name(k));
+      return v;
+    }
+    fail("expected make_" + std::string(ty.base == 'f' ? "float" : ty.base == 'u' ? "uint" : "int") +
+             std::to_string(ty.width) + "(..) or a vector variable",
+         p);
+  }
+
+  // `name = <vector expression>` as MK+ statements (without the final ';')
+  std::string vector_assign(const std::string& name, CT ty, Pos p) {
+    if (at_vector_ref()) {
+      auto [arr, idx, vt] = vector_ref();
+      if (vt.width != ty.width || (vt.base == 'f') != (ty.base == 'f')) fail("vector type mismatch", p);
+      std::string o = "vload(" + arr + ", " + idx;
+      for (int k = 0; k < ty.width; ++k) o += ", " + name + "_" + comp_name(k);
+      return o + ");";
+    }
+    std::vector<std::string> vals = vector_value(ty, p);
+    std::string o;
+    for (int k = 0; k < ty.width; ++k)
+      o += (k ? " " : "") + name + "_" + comp_name(k) + " = " + vals[size_t(k)] + ";";
+    return o;
+  }
+
+  // ---- statements --------------------------------------------------------------------------
   void for_loop(const std::string& unroll) {
     Pos p = next().pos;  // for
     want_op("(");
     std::string init;
     if (at_type()) {
-      std::string ty = type_name();
+      CT ty = type_name();
+      if (ty.width > 1) fail("vector loop variables are outside the subset", p);
       CTok n = want_id();
       want_op("=");
-      init = ty + " " + n.t + " = " + expr().t;
+      vars_[n.t] = ty.base;
+      vecs_.erase(n.t);
+      init = std::string(mk_type(ty.base)) + " " + n.t + " = " + conv(expr(), ty.base, n.pos).t;
       if (is_op(",")) fail("one loop variable per for in the CUDA subset", peek().pos);
     } else if (!is_op(";")) {
       init = simple();
@@ -535,15 +732,33 @@ class Translator {
     body_stmt();
   }
 
-  std::string lvalue() {
+  // name | name[i] | vec.c  -> (MK+ text, type)
+  std::pair<std::string, char> lvalue() {
     CTok n = want_id();
     if (is_op("[")) {
       next();
       CE i = expr();
       want_op("]");
-      return n.t + "[" + i.t + "]";
+      auto it = arrs_.find(n.t);
+      return {n.t + "[" + conv(i, 'i', n.pos).t + "]", it == arrs_.end() ? 'i' : it->second};
     }
-    return n.t;
+    if (is_op(".")) {
+      auto it = vecs_.find(n.t);
+      if (it == vecs_.end()) fail("member access is outside the CUDA subset", peek().pos);
+      next();
+      CTok c = want_id();
+      int k = component(c, it->second);
+      return {n.t + "_" + comp_name(k), it->second.base};
+    }
+    if (vecs_.count(n.t)) fail("a whole vector is not a scalar lvalue", n.pos);
+    auto it = vars_.find(n.t);
+    return {n.t, it == vars_.end() ? 'i' : it->second};
+  }
+
+  int component(const CTok& c, CT ty) {
+    for (int k = 0; k < ty.width; ++k)
+      if (c.t == comp_name(k)) return k;
+    fail("no component '" + c.t + "' in a " + std::to_string(ty.width) + "-vector", c.pos);
   }
 
   // assignment / compound assignment / ++ / -- / call, without the terminator
@@ -551,32 +766,36 @@ class Translator {
     Pos p = peek().pos;
     if (is_op("++") || is_op("--")) {
       std::string op = next().t == "++" ? "+" : "-";
-      std::string lv = lvalue();
+      auto [lv, lt] = lvalue();
       return lv + " = " + lv + " " + op + " 1";
     }
     if (peek().k == CTok::Id && is_op("(", 1)) {
       CE e = expr();
       return e.t;
     }
-    std::string lv = lvalue();
+    auto [lv, lt] = lvalue();
     if (is_op("++") || is_op("--")) {
       std::string op = next().t == "++" ? "+" : "-";
       return lv + " = " + lv + " " + op + " 1";
     }
     if (is_op("=")) {
       next();
-      return lv + " = " + expr().t;
+      return lv + " = " + conv(expr(), lt, p).t;
     }
     static const std::set<std::string> compound = {"+=", "-=", "*=", "/=", "%=", "<<=", ">>=", "&=", "|=", "^="};
     if (peek().k == CTok::Op && compound.count(peek().t)) {
       std::string op = next().t;
       op.pop_back();
-      return lv + " = " + lv + " " + op + " (" + expr().t + ")";
+      CE r = expr();
+      CE l{lv, lt};
+      // the compound form keeps C's x = x op (e): parenthesized right operand
+      r.t = "(" + r.t + ")";
+      return lv + " = " + conv(binary(op, l, r, p), lt, p).t;
     }
     fail("expected an assignment, found '" + peek().t + "'", p);
   }
 
-  // ---- expressions (C precedence; every binary node parenthesized) ----
+  // ---- expressions (C precedence and usual arithmetic conversions) -------------------------
   static int prec(const std::string& op) {
     static const std::map<std::string, int> m = {{"||", 1}, {"&&", 2}, {"|", 3},  {"^", 4},  {"&", 5},
                                                   {"==", 6}, {"!=", 6}, {"<", 7},  {"<=", 7}, {">", 7},
@@ -584,6 +803,62 @@ class Translator {
                                                   {"*", 10}, {"/", 10}, {"%", 10}};
     auto it = m.find(op);
     return it == m.end() ? 0 : it->second;
+  }
+
+  // value of `e` as type `to` (C's implicit conversions restricted to the exact ones)
+  CE conv(const CE& e, char to, Pos p) {
+    if (e.ty == to) return e;
+    if (to == 'f') {
+      if (e.ty == 'u') fail("unsigned -> float conversion is outside the CUDA subset", p);
+      return CE{e.t, 'f'};  // int -> float is implicit in Mini-Kernel too (same IR as a .mk source)
+    }
+    if (e.ty == 'f') {
+      if (to == 'u') fail("float -> unsigned conversion is outside the CUDA subset", p);
+      return CE{"int(" + e.t + ")", 'i'};
+    }
+    return CE{e.t, to};  // int <-> unsigned: the same 32-bit word
+  }
+
+  static std::optional<int> pow2_const(const std::string& t) {
+    std::string s = t;
+    uint64_t v;
+    if (s.rfind("0x", 0) == 0 || s.rfind("0X", 0) == 0) v = std::strtoull(s.c_str() + 2, nullptr, 16);
+    else if (!s.empty() && std::isdigit(static_cast<unsigned char>(s[0])) &&
+             s.find_first_not_of("0123456789") == std::string::npos)
+      v = std::strtoull(s.c_str(), nullptr, 10);
+    else
+      return std::nullopt;
+    if (v == 0 || (v & (v - 1)) != 0 || v > (1ull << 31)) return std::nullopt;
+    int k = 0;
+    while ((1ull << k) != v) ++k;
+    return k;
+  }
+
+  CE binary(const std::string& op, CE l, CE r, Pos p) {
+    bool cmp = op == "<" || op == "<=" || op == ">" || op == ">=" || op == "==" || op == "!=";
+    if (op == "&&" || op == "||") return CE{"(" + l.t + " " + op + " " + r.t + ")", 'i'};
+    if (op == "<<" || op == ">>") {
+      if (l.ty == 'f' || r.ty == 'f') fail("shifts of float operands", p);
+      if (op == ">>" && l.ty == 'u') return CE{"shr_u(" + l.t + ", " + r.t + ")", 'u'};
+      return CE{"(" + l.t + " " + op + " " + r.t + ")", l.ty};
+    }
+    char t = (l.ty == 'f' || r.ty == 'f') ? 'f' : (l.ty == 'u' || r.ty == 'u') ? 'u' : 'i';
+    if (t == 'f' && (l.ty == 'u' || r.ty == 'u')) fail("mixing unsigned and float is outside the CUDA subset", p);
+    if (t == 'u') {
+      if (op == "<") return CE{"ltu(" + l.t + ", " + r.t + ")", 'i'};
+      if (op == ">") return CE{"ltu(" + r.t + ", " + l.t + ")", 'i'};
+      if (op == "<=") return CE{"(ltu(" + r.t + ", " + l.t + ") == 0)", 'i'};
+      if (op == ">=") return CE{"(ltu(" + l.t + ", " + r.t + ") == 0)", 'i'};
+      if (op == "/" || op == "%") {
+        auto k = pow2_const(r.t);
+        if (!k) fail("unsigned / and % are supported by a power-of-two constant only", p);
+        if (op == "/") return CE{"shr_u(" + l.t + ", " + std::to_string(*k) + ")", 'u'};
+        return CE{"(" + l.t + " & " + std::to_string((1ll << *k) - 1) + ")", 'u'};
+      }
+    }
+    if (op == "%" && t == 'f') fail("% of float operands", p);
+    if ((op == "&" || op == "|" || op == "^") && t == 'f') fail("bitwise operators on float operands", p);
+    return CE{"(" + l.t + " " + op + " " + r.t + ")", cmp ? 'i' : t};
   }
 
   CE expr(int min_prec = 1) {
@@ -595,9 +870,9 @@ class Translator {
         fail("assignments inside expressions are outside the CUDA subset", peek().pos);
       int pr = prec(op);
       if (pr < min_prec || pr == 0) break;
-      next();
+      Pos p = next().pos;
       CE r = expr(pr + 1);
-      l.t = "(" + l.t + " " + op + " " + r.t + ")";
+      l = binary(op, l, r, p);
     }
     return l;
   }
@@ -607,7 +882,8 @@ class Translator {
     if (t.k == CTok::Op) {
       if (t.t == "-") {
         next();
-        return CE{"(-" + unary().t + ")"};
+        CE e = unary();
+        return CE{"(-" + e.t + ")", e.ty};
       }
       if (t.t == "+") {
         next();
@@ -615,42 +891,53 @@ class Translator {
       }
       if (t.t == "!") {
         next();
-        return CE{"(!" + unary().t + ")"};
+        return CE{"(!" + unary().t + ")", 'i'};
       }
       if (t.t == "~") {
         next();
-        return CE{"(" + unary().t + " ^ (-1))"};
+        CE e = unary();
+        if (e.ty == 'f') fail("~ of a float operand", t.pos);
+        return CE{"(" + e.t + " ^ (-1))", e.ty};
       }
       if (t.t == "++" || t.t == "--") fail("++/-- inside expressions are outside the CUDA subset", t.pos);
       if (t.t == "&" || t.t == "*") fail("address-of / dereference are outside the CUDA subset", t.pos);
       if (t.t == "(") {
         // cast or parenthesized expression
-        if ((is_id("int", 1) || is_id("float", 1)) && is_op(")", 2)) {
+        size_t o = 1;
+        while (peek(o).k == CTok::Id && is_qualifier(peek(o).t)) ++o;
+        if (peek(o).k == CTok::Id && type_word(peek(o).t) && !at_vector_ref()) {
           next();
-          std::string ty = next().t;
-          next();
-          return CE{ty + "(" + unary().t + ")"};
+          Pos cp = peek().pos;
+          CT ty = type_name();
+          if (ty.width > 1 || is_op("*")) fail("pointer / vector casts must index an array", cp);
+          want_op(")");
+          CE e = unary();
+          if (ty.base == 'f') {
+            if (e.ty == 'u') fail("unsigned -> float conversion is outside the CUDA subset", cp);
+            return CE{"float(" + e.t + ")", 'f'};
+          }
+          if (e.ty == 'f') {
+            if (ty.base == 'u') fail("float -> unsigned conversion is outside the CUDA subset", cp);
+            return CE{"int(" + e.t + ")", 'i'};
+          }
+          return CE{e.t, ty.base};
         }
-        if (peek(1).k == CTok::Id && (peek(1).t == "unsigned" || peek(1).t == "double" || peek(1).t == "long"))
+        if (peek(1).k == CTok::Id && (peek(1).t == "double" || peek(1).t == "long"))
           fail("cast to '" + peek(1).t + "' is outside the CUDA subset", t.pos);
+        if (at_vector_ref()) fail("a vector load must initialize or be assigned to a vector variable", t.pos);
         next();
         CE e = expr();
         want_op(")");
         return e;
       }
     }
+    if (at_vector_ref()) fail("a vector load must initialize or be assigned to a vector variable", t.pos);
     return postfix(primary());
   }
 
   CE postfix(CE e) {
-    while (is_op("[")) {
-      next();
-      CE i = expr();
-      want_op("]");
-      e.t += "[" + i.t + "]";
-    }
     if (is_op("++") || is_op("--")) fail("++/-- inside expressions are outside the CUDA subset", peek().pos);
-    if (is_op(".") || is_op("->")) fail("member access is outside the CUDA subset", peek().pos);
+    if (is_op("->")) fail("member access is outside the CUDA subset", peek().pos);
     return e;
   }
 
@@ -666,34 +953,50 @@ class Translator {
     return a;
   }
 
+  CE literal(const CTok& t) {
+    std::string s = t.t;
+    bool uns = !s.empty() && s.back() == 'u';
+    if (uns) s.pop_back();
+    bool hex = s.size() > 2 && (s[1] == 'x' || s[1] == 'X');
+    uint64_t v = hex ? std::strtoull(s.c_str() + 2, nullptr, 16) : std::strtoull(s.c_str(), nullptr, 10);
+    if (v > 0xffffffffull || (hex && s.size() - 2 > 8)) fail("integer literal wider than 32 bits", t.pos);
+    if (!uns && !hex && v > 2147483647ull) fail("integer literal out of int32 range (long in C)", t.pos);
+    char ty = (uns || v > 2147483647ull) ? 'u' : 'i';
+    if (v > 2147483647ull || hex) {
+      char buf[16];
+      std::snprintf(buf, sizeof(buf), "0x%08llx", static_cast<unsigned long long>(v));
+      return CE{buf, ty};
+    }
+    return CE{s, ty};
+  }
+
   CE primary() {
     CTok t = next();
-    if (t.k == CTok::Int) {
-      if (t.t.size() > 2 && (t.t[1] == 'x' || t.t[1] == 'X')) {
-        if (t.t.size() - 2 > 8) fail("hex literal wider than 32 bits", t.pos);
-        return CE{t.t};
-      }
-      long long v = std::strtoll(t.t.c_str(), nullptr, 10);
-      if (v > 2147483647LL) fail("integer literal out of int32 range", t.pos);
-      return CE{t.t};
-    }
-    if (t.k == CTok::Flt) return CE{t.t};
+    if (t.k == CTok::Int) return literal(t);
+    if (t.k == CTok::Flt) return CE{t.t, 'f'};
     if (t.k != CTok::Id) fail("expected an expression, found '" + t.t + "'", t.pos);
     static const std::set<std::string> builtins = {"threadIdx", "blockIdx", "blockDim", "gridDim"};
     if (builtins.count(t.t)) {
       want_op(".");
       CTok f = want_id();
       if (f.t != "x" && f.t != "y" && f.t != "z") fail("unknown builtin component '" + f.t + "'", f.pos);
-      return CE{t.t + "." + f.t};
+      return CE{t.t + "." + f.t, 'i'};
     }
-    if (t.t == "warpSize") return CE{"32"};
+    if (t.t == "warpSize") return CE{"32", 'i'};
     if (is_op("(")) {
       if (t.t == "atomicAdd")
         fail("the result of atomicAdd cannot be used in the CUDA subset (use it as a statement)", t.pos);
       if (t.t == "fminf" || t.t == "fabsf" || t.t == "sqrtf" || t.t == "expf" || t.t == "atomicMin" ||
-          t.t == "atomicMax" || t.t == "atomicCAS" || t.t == "atomicExch" ||
+          t.t == "atomicMax" || t.t == "atomicCAS" || t.t == "atomicExch" || t.t == "__umulhi" ||
           (t.t.rfind("__shfl", 0) == 0 && t.t != "__shfl_xor_sync"))
         fail("'" + t.t + "' is outside the CUDA subset", t.pos);
+      if (t.t == "__ldg") {  // __ldg(&a[i]) -> a[i] (read-only arrays are const __restrict__ already)
+        want_op("(");
+        want_op("&");
+        auto [lv, lt] = lvalue();
+        want_op(")");
+        return CE{lv, lt};
+      }
       std::vector<CE> a = call_args();
       auto arity = [&](size_t n) {
         if (a.size() != n) fail(t.t + " takes " + std::to_string(n) + " argument(s)", t.pos);
@@ -702,25 +1005,60 @@ class Translator {
         arity(3);
         if (a[0].t != "0xffffffff" && a[0].t != "(-1)")
           fail("__shfl_xor_sync is supported with the full mask 0xffffffff only", t.pos);
-        return CE{"warp_shfl_xor(" + a[1].t + ", " + a[2].t + ")"};
+        return CE{"warp_shfl_xor(" + a[1].t + ", " + a[2].t + ")", a[1].ty};
       }
       if (t.t == "__float2int_rz") {
         arity(1);
-        return CE{"int_rz(" + a[0].t + ")"};
+        return CE{"int_rz(" + a[0].t + ")", 'i'};
       }
       if (t.t == "__funnelshift_r" || t.t == "__funnelshift_l") {
         arity(3);
-        return CE{std::string(t.t == "__funnelshift_r" ? "fshr(" : "fshl(") + a[0].t + ", " + a[1].t + ", " + a[2].t + ")"};
+        return CE{std::string(t.t == "__funnelshift_r" ? "fshr(" : "fshl(") + a[0].t + ", " + a[1].t + ", " +
+                      a[2].t + ")",
+                  'u'};
       }
       if (t.t == "int" || t.t == "float") {
         arity(1);
-        return CE{t.t + "(" + a[0].t + ")"};
+        return conv(a[0], t.t == "float" ? 'f' : 'i', t.pos);
+      }
+      if (t.t == "min" || t.t == "max") {
+        arity(2);
+        if (a[0].ty == 'u' || a[1].ty == 'u') {
+          if (a[0].ty == 'f' || a[1].ty == 'f') fail("mixing unsigned and float is outside the CUDA subset", t.pos);
+          // unsigned min/max: a ^ ((a ^ b) & -(b <u a))  /  a ^ ((a ^ b) & -(a <u b))
+          std::string sel = t.t == "min" ? "ltu(" + a[1].t + ", " + a[0].t + ")" : "ltu(" + a[0].t + ", " + a[1].t + ")";
+          return CE{"(" + a[0].t + " ^ ((" + a[0].t + " ^ " + a[1].t + ") & (0 - " + sel + ")))", 'u'};
+        }
+        char ty = (a[0].ty == 'f' || a[1].ty == 'f') ? 'f' : 'i';
+        return CE{t.t + "(" + a[0].t + ", " + a[1].t + ")", ty};
+      }
+      if (t.t == "fmaxf") {
+        arity(2);
+        return CE{"fmaxf(" + conv(a[0], 'f', t.pos).t + ", " + conv(a[1], 'f', t.pos).t + ")", 'f'};
       }
       std::string o = t.t + "(";
       for (size_t i = 0; i < a.size(); ++i) o += (i ? ", " : "") + a[i].t;
-      return CE{o + ")"};
+      auto f = funcs_.find(t.t);
+      return CE{o + ")", f == funcs_.end() ? 'i' : f->second};
     }
-    return CE{t.t};
+    if (is_op("[")) {
+      next();
+      CE i = expr();
+      want_op("]");
+      auto it = arrs_.find(t.t);
+      return CE{t.t + "[" + conv(i, 'i', t.pos).t + "]", it == arrs_.end() ? 'i' : it->second};
+    }
+    if (is_op(".")) {
+      auto it = vecs_.find(t.t);
+      if (it == vecs_.end()) fail("member access is outside the CUDA subset", peek().pos);
+      next();
+      CTok c = want_id();
+      int k = component(c, it->second);
+      return CE{t.t + "_" + comp_name(k), it->second.base};
+    }
+    if (vecs_.count(t.t)) fail("a whole vector cannot be used as a scalar", t.pos);
+    auto it = vars_.find(t.t);
+    return CE{t.t, it == vars_.end() ? 'i' : it->second};
   }
 
   // Constant folding of a translated expression (shared lengths, launch bounds).

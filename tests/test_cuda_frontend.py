@@ -142,7 +142,10 @@ def test_cuda_features_lower_and_run_on_reference_interpreter(hf, tmp_path):
     ("  int v = t > 0 ? 1 : 2;\n", 3, "?:"),
     ("  float a[4];\n", 3, "local arrays"),
     ("  for (int i = 0; i < 4; ++i) { break; }\n", 3, "break"),
-    ("  unsigned int u = 3;\n", 3, "unsigned"),
+    ("  double u = 3;\n", 3, "double"),
+    ("  unsigned u = 3u; float f = u;\n", 3, "unsigned -> float"),
+    ("  unsigned u = 3u; u = u / 3u;\n", 3, "power-of-two"),
+    ("  float4 v = reinterpret_cast<const float4*>(c)[0];\n", 3, "element type"),
     ("  int v = atomicAdd(&c[0], 1);\n", 3, "atomicAdd"),
     ("  float v = __shfl_xor_sync(0x0000ffff, 1.0f, 1);\n", 3, "full mask"),
     ("  int* p = c;\n", 3, "pointers"),
@@ -176,3 +179,115 @@ def test_cuda_corpus_pair_on_device(gpu, corpus):
         mod.run(img)
         img.download()
         assert img.digest_hex() == want["sequential"], f"seed {seed}"
+
+
+UNSIGNED = r"""
+__device__ unsigned rotr(unsigned x, int n) { return (x >> n) | (x << (32 - n)); }
+
+//@ grid=1
+__global__ void __launch_bounds__(64) words(const uint32_t* __restrict__ in, uint32_t* out, int* flags) {
+  int t = threadIdx.x;
+  uint32_t a = in[t], b = in[(t + 1) % 64];
+  unsigned int s = a + b * 2654435761u;
+  s ^= rotr(s, 13);
+  s += 0x9e3779b9;
+  out[t] = s;
+  out[64 + t] = a >> 7;
+  out[128 + t] = a / 16u + a % 8u;
+  out[192 + t] = min(a, b) ^ max(a, b);
+  out[256 + t] = __funnelshift_r(a, b, 5);
+  flags[t] = (a < b) + 2 * (a >= 0x80000000u) + 4 * (b <= a) + 8 * (a > 7u);
+}
+"""
+
+
+def unsigned_reference(x):
+    x = np.asarray(x, np.uint64)
+    b = np.roll(x, -1)
+    M = 0xFFFFFFFF
+    s = (x + b * 2654435761) & M
+    s ^= ((s >> 13) | (s << 19)) & M
+    s = (s + 0x9E3779B9) & M
+    out = np.concatenate([s, x >> 7, (x // 16 + x % 8) & M, np.minimum(x, b) ^ np.maximum(x, b),
+                          ((x | (b << 32)) >> 5) & M])
+    flags = (x < b).astype(np.int64) + 2 * (x >= 0x80000000) + 4 * (b <= x) + 8 * (x > 7)
+    return out.astype(np.uint32), flags
+
+
+VECTORS = r"""
+//@ grid=2
+__global__ void __launch_bounds__(32) vec(const float* __restrict__ x, float* y, const int* __restrict__ k,
+                                          int* m) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  float4 v = reinterpret_cast<const float4*>(x)[t];
+  float4 w;
+  w = make_float4(v.w, v.z + 1.0f, v.y * 2.0f, v.x);
+  w.x += __ldg(&x[0]);
+  reinterpret_cast<float4*>(y)[t] = w;
+  int2 q = ((const int2*)k)[t];
+  reinterpret_cast<int2*>(m)[t] = make_int2(q.y, q.x - q.y);
+}
+"""
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_cuda_unsigned_and_vectors_on_reference_interpreter(hf, tmp_path):
+    """uint32_t arithmetic (shr_u, ltu, power-of-two / and %, unsigned min/max, wide literals,
+    funnel shifts) and float4/int2 loads, stores, components: lowered to Mini-Kernel, run on the
+    reference interpreter, equal to numpy's uint32 / float32 semantics."""
+    for src, img, check in [
+        (UNSIGNED, "array in int32 64 seed 11 range -2147483648 2147483647\narray out int32 320 zero\n"
+                   "array flags int32 64 zero\n", "u"),
+        (VECTORS, "array x float32 256 seed 5 uniform -1 1\narray y float32 256 zero\n"
+                  "array k int32 128 seed 6 range -1000 1000\narray m int32 128 zero\n", "v")]:
+        assert hf.check(src).startswith("ok")
+        (tmp_path / "k.mk").write_text(hf.lower(src))
+        (tmp_path / "k.img").write_text(img)
+        grid = 1 if check == "u" else 2
+        _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img", "--grid", grid)
+        arrays, _ = oracle.parse_image(dump)
+        inputs, _ = oracle.parse_image(img)
+        if check == "u":
+            want, flags = unsigned_reference(np.asarray(inputs["in"], np.int64) & 0xFFFFFFFF)
+            assert np.array_equal(np.asarray(arrays["out"]).astype(np.int64) & 0xFFFFFFFF, want.astype(np.int64))
+            assert [int(v) for v in arrays["flags"]] == [int(v) for v in flags]
+        else:
+            x = np.asarray(inputs["x"], np.float32).reshape(-1, 4)[:64]
+            y = np.stack([x[:, 3], x[:, 2] + np.float32(1), x[:, 1] * np.float32(2), x[:, 0]], 1)
+            y[:, 0] = y[:, 0] + np.float32(inputs["x"][0])
+            got = np.asarray(arrays["y"], np.float32).reshape(-1, 4)[:64]
+            assert np.array_equal(got.view(np.uint32), y.astype(np.float32).view(np.uint32))
+            q = np.asarray(inputs["k"], np.int64).reshape(-1, 2)[:64]
+            assert [int(v) for v in np.asarray(arrays["m"]).reshape(-1, 2)[:64].ravel()] == \
+                [int(v) for v in np.stack([q[:, 1], q[:, 0] - q[:, 1]], 1).ravel()]
+        m = hf.Module.kernel(src, grid=grid)  # and the sm_100a emission compiles (NVRTC)
+        assert len(m.cubin) > 1000
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_cuda_b200_hist_member_equals_the_mkplus_member(hf, tmp_path):
+    """The bench's vectorized Hist member written in CUDA (float4 loads, __float2int_rz, shared
+    atomics) gives the MK+ member's bins on the reference interpreter (ragged and parity n)."""
+    from paper_2007_01277_b200 import pairs
+    for n in (1001, 2 * 8 * 56 * 56):
+        digs = []
+        for src in (cu("histogram_b200.cu"), pairs.source("b200", "histogram")):
+            (tmp_path / "k.mk").write_text(hf.lower(src))
+            (tmp_path / "k.img").write_text(pairs._hist(n, -4.5, 4.5)(0).image)
+            digs.append(oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img", "--grid", 4)[0])
+        assert digs[0] == digs[1], n
+
+
+@pytest.mark.gpu
+def test_cuda_member_fused_with_mkplus_member_on_device(gpu):
+    """Mixed input languages: the CUDA Hist fused with the MK+ BatchNorm at 512/512 reproduces
+    the reference's sequential run of the MK+ pair (members.json fixture) bit for bit."""
+    from paper_2007_01277_b200 import pairs
+    hf = gpu
+    G = golden("members.json")
+    m = hf.Module.fused(pairs.source("b200", "batchnorm"), cu("histogram_b200.cu"), 512, 512, grid=G["grid"])
+    img = hf.Image(pairs.MEMBERS["bn"].sizes["parity"](0).image).merge(
+        hf.Image(pairs.MEMBERS["hist"].sizes["parity"](0).image)).upload()
+    m.run(img, G["grid"])
+    img.download()
+    assert img.digest_hex() == G["pairs"]["bn+hist"]["512"]["digest"]
