@@ -45,6 +45,11 @@ class Checker {
   std::vector<std::map<std::string, Sym>> scopes_;
   const Func* fn_ = nullptr;
   bool in_kernel_ = false;
+  bool bcast_ok_ = false;  // the expression being typed is a whole assignment value
+
+  static std::optional<int32_t> const_int(const Expr& e) {
+    return eval_scalar_int(e, [](const std::string&) -> std::optional<int32_t> { return std::nullopt; });
+  }
 
   static std::vector<std::string> callees(const Block& b) {
     std::vector<std::string> out;
@@ -168,6 +173,16 @@ class Checker {
               raise(Code::TypeMismatch, std::string(intr_name(Intr(e.i))) + " takes an array element", e.a[0].pos);
             return type(e.a[0]);
           case Intr::CastFloat: type(e.a[0]); return Ty::Float;
+          case Intr::Bcast: {
+            if (!bcast_ok_)
+              raise(Code::TypeMismatch, "warp_bcast must be the whole right-hand side of an assignment", e.pos);
+            bcast_ok_ = false;
+            auto w = const_int(e.a[2]);
+            if (!w || *w < 2 || *w > 32 || (*w & (*w - 1)) != 0)
+              raise(Code::TypeMismatch, "warp_bcast width must be a constant power of two in [2, 32]", e.a[2].pos);
+            if (type(e.a[1]) != Ty::Int) raise(Code::TypeMismatch, "warp_bcast source lane must be int", e.a[1].pos);
+            return type(e.a[0]);
+          }
           case Intr::Fmaxf:
             type(e.a[0]);
             type(e.a[1]);
@@ -254,7 +269,10 @@ class Checker {
         break;
       case SK::Assign: {
         Ty t = target(s);
-        assignable(t, type(s.val[0]), s.pos);
+        const Expr& v = s.val[0];
+        bcast_ok_ = v.k == EK::Intrin && Intr(v.i) == Intr::Bcast && s.idx.empty();
+        assignable(t, type(v), s.pos);
+        bcast_ok_ = false;
         break;
       }
       case SK::If:

@@ -866,6 +866,7 @@ class Parser {
           else if (b200() && n.text == "int_rz") w = Intr::IntRz;
           else if (b200() && n.text == "load_acquire") w = Intr::Acquire;
           else if (b200() && n.text == "load_relaxed") w = Intr::Relaxed;
+          else if (b200() && n.text == "warp_bcast") w = Intr::Bcast;
           if (w) {
             std::vector<Expr> a = args();
             if (int(a.size()) != intr_arity(*w))

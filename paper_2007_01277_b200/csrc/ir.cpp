@@ -42,6 +42,7 @@ const char* intr_name(Intr i) {
     case Intr::IntRz: return "int_rz";
     case Intr::Acquire: return "load_acquire";
     case Intr::Relaxed: return "load_relaxed";
+    case Intr::Bcast: return "warp_bcast";
   }
   return "?";
 }
@@ -50,7 +51,7 @@ int intr_arity(Intr i) {
   if (i == Intr::CastInt || i == Intr::CastFloat || i == Intr::IntRz || i == Intr::Acquire ||
       i == Intr::Relaxed)
     return 1;
-  if (i == Intr::Fshr || i == Intr::Fshl) return 3;
+  if (i == Intr::Fshr || i == Intr::Fshl || i == Intr::Bcast) return 3;
   return 2;
 }
 

@@ -70,6 +70,8 @@ enum class Intr : uint8_t {
   IntRz,  // int_rz(x): int(x) for |x| < 2^31 (device: one cvt.rzi.s32); outside that range undefined
   Acquire,  // load_acquire(a[i]): a[i] read with gpu-scope acquire (pairs with atomic_add_release)
   Relaxed,  // load_relaxed(a[i]): gpu-scope strong read, no ordering (a later fence() acquires)
+  Bcast,    // x = warp_bcast(v, src, w): v of lane (lane & ~(w-1)) + src; w a constant power of two
+            // in [2, 32], src uniform within each w-lane group; only as a whole assignment value
 };
 const char* intr_name(Intr i);
 int intr_arity(Intr i);

@@ -635,7 +635,8 @@ Expr shr_u(const Expr& x, const Expr& n) {
 
 struct Lowerer {
   int counter = 0;
-  std::map<std::string, Ty> arrays;  // params + shared
+  std::map<std::string, Ty> arrays;   // params + shared
+  std::map<std::string, Ty> scalars;  // params + declared locals (types of warp_bcast targets)
 
   Expr expr(const Expr& e) {
     Expr c = e;
@@ -708,6 +709,38 @@ struct Lowerer {
     }
     c.body = block(c.body);
     c.alt = block(c.alt);
+    if (c.k == SK::Decl) scalars[c.name] = c.ty;
+    if (c.k == SK::Assign && c.idx.empty() && c.val[0].k == EK::Intrin && Intr(c.val[0].i) == Intr::Bcast) {
+      // x = warp_bcast(v, src, w): the xor butterfly the interpreter executes in lock step --
+      // every lane shuffles at each step, a lane whose group index differs from src in bit m
+      // adopts its partner's value (exact when src is uniform within each w-lane group)
+      const Expr& b = c.val[0];
+      int w = 2;
+      if (auto k = const_of(b.a[2])) w = *k;
+      int id = counter++;
+      std::string src = "__bs" + std::to_string(id);
+      Ty t = scalars.count(c.name) ? scalars[c.name] : Ty::Int;
+      out.push_back(assign(c.name, b.a[0]));
+      out.push_back(decl_init(Ty::Int, src, b.a[1]));
+      Expr tid = binary(Bin::Add, builtin(Builtin::TidX),
+                        binary(Bin::Add, binary(Bin::Mul, builtin(Builtin::TidY), builtin(Builtin::BdimX)),
+                               binary(Bin::Mul, builtin(Builtin::TidZ),
+                                      binary(Bin::Mul, builtin(Builtin::BdimX), builtin(Builtin::BdimY)))));
+      for (int m = 1; m < w; m <<= 1) {
+        std::string tmp = "__bt" + std::to_string(id) + "_" + std::to_string(m);
+        Expr sh;
+        sh.k = EK::Shfl;
+        sh.i = m;
+        sh.a.push_back(var(c.name));
+        sh.pos = c.pos;
+        out.push_back(decl_init(t, tmp, sh));
+        Expr differs = binary(Bin::Ne,
+                              binary(Bin::And, binary(Bin::Xor, binary(Bin::Mod, tid, lit(32)), var(src)), lit(m)),
+                              lit(0));
+        out.push_back(if_(differs, Block{assign(c.name, var(tmp))}));
+      }
+      return;
+    }
     if (c.k == SK::Fence) return;     // the interpreter is sequentially consistent
     if (c.k == SK::Atomic) c.bid = 0;  // atomic_add_release -> atomic_add (same reason)
     if (c.k == SK::WarpSync) return;  // ... and runs each warp in lock step
@@ -741,6 +774,7 @@ Kernel downlower(const Kernel& k) {
   Lowerer l;
   for (const auto& p : k.params)
     if (p.array) l.arrays[p.name] = p.ty;
+    else l.scalars[p.name] = p.ty;
   for (const auto& sh : k.shared) l.arrays[sh.name] = sh.ty;
   Kernel out = k;
   out.body = l.block(k.body);
@@ -755,6 +789,7 @@ Program downlower(const Program& p) {
     Lowerer l;
     for (const auto& prm : f.params)
       if (prm.array) l.arrays[prm.name] = prm.ty;
+      else l.scalars[prm.name] = prm.ty;
     f.body = l.block(f.body);
   }
   return out;

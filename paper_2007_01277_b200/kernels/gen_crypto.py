@@ -457,14 +457,10 @@ def absorb_words(src, A, words):
 
 
 def bcast8(src, var, lane_src, tmp="bt"):
-    """Broadcast `var` from group lane `lane_src` (0..7, static or a variable) to the 8 lanes of each
-    8-lane group with a 3-step xor butterfly: at step m a lane whose bit m differs from the
-    source's adopts its partner's value (lj = lane % 8)."""
-    for m in (1, 2, 4):
-        src(f"{tmp} = warp_shfl_xor({var}, {m});")
-        src(f"if (((lj ^ {lane_src}) & {m}) != 0) {{")
-        src(f"  {var} = {tmp};")
-        src("}")
+    """Broadcast `var` from group lane `lane_src` (0..7, the same for the 8 lanes of a group) to
+    the 8 lanes of each 8-lane group: MK+ warp_bcast, one shfl.idx on the B200 (its lowering for
+    the interpreter is the 3-step xor butterfly this helper used to spell out)."""
+    src(f"{var} = warp_bcast({var}, {lane_src}, 8);")
 
 
 def gen_ethash():
@@ -479,7 +475,7 @@ def gen_ethash():
 // B200 mechanics (ethminer's lane-cooperative layout): every thread computes the two Keccaks
 // of its own nonce, but the DAG loop of the 8 nonces of an 8-lane group is shared: lane j
 // holds words 4j..4j+3 of """ + str(HPP) + """ of the group's mixes at a time, the lane owning mix[i % 32]
-// computes each page index and broadcasts it (xor-butterfly shuffles), and each DAG page is
+// computes each page index and broadcasts it (warp_bcast: one shfl.idx), and each DAG page is
 // read by the 8 lanes as one coalesced 128-byte segment (""" + str(HPP) + """ pages in flight per lane
 // per round, 4 lines per warp load instead of 32; 8 in flight measured 7% faster than 4 on B200). Keccak-f[1600] lanes are 32-bit halves (funnel-shift rotates, chi as
 // LOP3, rho+pi in place along the pi cycle, chi row by row: ~64 live registers), 24 rounds as

@@ -16,20 +16,22 @@ o.append(f"Geomean speedup vs min(seq, two-stream): {d['speedup_geomean']:.3f}. 
          f"{d['value']:.1f} µs fused vs {d['unfused_two_stream_step_us']:.1f} µs unfused on two streams. "
          f"e2e (host buffers, pipelined): {d['e2e']['value'] / 1000:.1f} ms per step "
          f"({d['e2e']['h2d_bytes_per_step'] / 1e9:.2f} GB up, {d['e2e']['d2h_bytes_per_step'] / 1e9:.2f} GB down); "
-         f"reference CPU interpreter: {d['cpu_baseline']['value'] / 1e6:.1f} s per step ({d['cpu_baseline']['cores']} processes). "
+         + (f"reference CPU interpreter: {d['cpu_baseline']['value'] / 1e6:.1f} s per step "
+            f"({d['cpu_baseline']['cores']} processes). " if d.get("cpu_baseline") else "") +
          f"Clocks {d['clocks']['sm_mhz']:.0f}/{d['clocks']['sm_max_mhz']:.0f} MHz, reasons {d['clocks']['reasons']}.")
-o.append("")
-o.append("| crypto pair | partition | registers | fused µs | seq µs | 2-stream µs | speedup | roofline (bound) |")
-o.append("|---|---|---|---|---|---|---|---|")
-for p in d["crypto"]["c3"]:
-    regs = ("budgets %d/%d" % tuple(p["interval_regs"])) if p.get("interval_regs") else (
-        "cap %s" % p["reg_cap"] if p["reg_cap"] else "uncapped (%d)" % p["regs"])
-    r = p.get("roofline") or {}
-    o.append(f"| {p['pair']} | {p['d1']}/{p['d2']} | {regs} | {p['fused_us']:.0f} | {p['seq_us']:.0f} | "
-             f"{p['two_stream_us']:.0f} | **{p['speedup']:.3f}** | {r.get('frac', 0):.2f} issue, {r.get('alu_frac', 0):.2f} ALU pipe |")
-c4 = d["crypto"]["c4"]
-b = c4["best"]
-o.append("")
-o.append(f"C4 Upsample + BLAKE-256: best d0 {b['d0']} (Upsample {b['d1']}), reg_cap {b['reg_cap']}: {b['us']:.1f} µs vs "
-         f"{c4['seq_us']:.1f} sequential / {c4['two_stream_us']:.1f} two-stream — **{c4['speedup']:.3f}×**.")
+if d.get("crypto"):
+    o.append("")
+    o.append("| crypto pair | partition | registers | fused µs | seq µs | 2-stream µs | speedup | roofline (bound) |")
+    o.append("|---|---|---|---|---|---|---|---|")
+    for p in d["crypto"]["c3"]:
+        regs = ("budgets %d/%d" % tuple(p["interval_regs"])) if p.get("interval_regs") else (
+            "cap %s" % p["reg_cap"] if p["reg_cap"] else "uncapped (%d)" % p["regs"])
+        r = p.get("roofline") or {}
+        o.append(f"| {p['pair']} | {p['d1']}/{p['d2']} | {regs} | {p['fused_us']:.0f} | {p['seq_us']:.0f} | "
+                 f"{p['two_stream_us']:.0f} | **{p['speedup']:.3f}** | {r.get('frac', 0):.2f} issue, {r.get('alu_frac', 0):.2f} ALU pipe |")
+    c4 = d["crypto"]["c4"]
+    b = c4["best"]
+    o.append("")
+    o.append(f"C4 Upsample + BLAKE-256: best d0 {b['d0']} (Upsample {b['d1']}), reg_cap {b['reg_cap']}: {b['us']:.1f} µs vs "
+             f"{c4['seq_us']:.1f} sequential / {c4['two_stream_us']:.1f} two-stream — **{c4['speedup']:.3f}×**.")
 print("\n".join(o))
