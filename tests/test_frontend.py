@@ -153,3 +153,45 @@ def test_release_acquire_handoff_constructs(hf):
         with pytest.raises(hf.HFuseError) as e:
             hf.emit_kernel(src) if code == "InvalidArgument" else hf.check(src)
         assert e.value.name == code
+
+
+BCAST = """kernel k(int xi[], int xo[], float fo[]) dims (64, 1, 1) {
+  int lane = threadIdx.x % 32;
+  int v = xi[threadIdx.x];
+  float f = float(v) * 0.5;
+  int g = lane / 8;
+  v = warp_bcast(v, (g + 3) % 8, 8);
+  f = warp_bcast(f, 5, 32);
+  xo[threadIdx.x] = v;
+  fo[threadIdx.x] = f;
+}
+"""
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_warp_bcast_lowering_on_reference_interpreter(hf, tmp_path):
+    """MK+ warp_bcast (group-uniform source lane): its butterfly lowering runs on the reference
+    interpreter and gives lane (lane & ~(w-1)) + src's value; the sm_100a emission is one
+    shfl.idx when the warp is full."""
+    import numpy as np
+    low = hf.lower(BCAST)
+    assert "warp_bcast" not in low and hf.check(low, strict=True).startswith("ok")
+    img = "array xi int32 64 seed 9 range -1000 1000\narray xo int32 64 zero\narray fo float32 64 zero\n"
+    (tmp_path / "k.mk").write_text(low)
+    (tmp_path / "k.img").write_text(img)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img")
+    arrays, _ = oracle.parse_image(dump)
+    xi = np.asarray(oracle.parse_image(img)[0]["xi"], np.int64)
+    t = np.arange(64)
+    src8 = (t & ~7) + (((t % 32) // 8 + 3) % 8) + (t // 32) * 0
+    assert [int(v) for v in arrays["xo"]] == [int(xi[(t0 & ~31) | (src8[t0] & 31)]) for t0 in t]
+    want_f = [np.float32(np.float32(xi[(t0 & ~31) + 5]) * np.float32(0.5)) for t0 in t]
+    assert np.array_equal(np.asarray(arrays["fo"], np.float32), np.asarray(want_f, np.float32))
+    cu = hf.emit_kernel(BCAST)
+    assert "hf_bcast(" in cu and "__shfl_sync(0xffffffffu, v, src, w)" in cu
+    with pytest.raises(hf.HFuseError) as e:
+        hf.check(BCAST.replace("v = warp_bcast(v, (g + 3) % 8, 8);", "v = 1 + warp_bcast(v, 1, 8);"))
+    assert e.value.name == "TypeMismatch" and "whole right-hand side" in e.value.message
+    with pytest.raises(hf.HFuseError) as e:
+        hf.check(BCAST.replace("(g + 3) % 8, 8)", "(g + 3) % 8, 6)"))
+    assert "power of two" in e.value.message
