@@ -867,11 +867,13 @@ class Parser {
           else if (b200() && n.text == "load_acquire") w = Intr::Acquire;
           else if (b200() && n.text == "load_relaxed") w = Intr::Relaxed;
           else if (b200() && n.text == "warp_bcast") w = Intr::Bcast;
+          else if (b200() && n.text == "addc") w = Intr::Addc;
           if (w) {
             std::vector<Expr> a = args();
             if (int(a.size()) != intr_arity(*w))
               raise(Code::Syntax, n.text + " takes exactly " +
-                                      std::string(intr_arity(*w) == 3 ? "three" : intr_arity(*w) == 1 ? "one" : "two") +
+                                      std::string(intr_arity(*w) == 4 ? "four" : intr_arity(*w) == 3 ? "three"
+                                                  : intr_arity(*w) == 1 ? "one" : "two") +
                                       " argument(s)", p);
             e = intrin(*w, std::move(a));
             e.pos = p;

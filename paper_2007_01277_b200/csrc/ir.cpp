@@ -43,6 +43,7 @@ const char* intr_name(Intr i) {
     case Intr::Acquire: return "load_acquire";
     case Intr::Relaxed: return "load_relaxed";
     case Intr::Bcast: return "warp_bcast";
+    case Intr::Addc: return "addc";
   }
   return "?";
 }
@@ -52,6 +53,7 @@ int intr_arity(Intr i) {
       i == Intr::Relaxed)
     return 1;
   if (i == Intr::Fshr || i == Intr::Fshl || i == Intr::Bcast) return 3;
+  if (i == Intr::Addc) return 4;
   return 2;
 }
 

@@ -72,6 +72,8 @@ enum class Intr : uint8_t {
   Relaxed,  // load_relaxed(a[i]): gpu-scope strong read, no ordering (a later fence() acquires)
   Bcast,    // x = warp_bcast(v, src, w): v of lane (lane & ~(w-1)) + src; w a constant power of two
             // in [2, 32], src uniform within each w-lane group; only as a whole assignment value
+  Addc,     // addc(ahi, bhi, alo, blo): ahi + bhi + carry-out of alo + blo (64-bit add, high word;
+            // device: add.cc + addc, i.e. IADD3 + IADD3.X instead of an unsigned compare)
 };
 const char* intr_name(Intr i);
 int intr_arity(Intr i);

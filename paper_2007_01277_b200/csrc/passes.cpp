@@ -665,6 +665,12 @@ struct Lowerer {
       }
       case Intr::LtU:
         return binary(Bin::Lt, binary(Bin::Xor, x, int_min()), binary(Bin::Xor, n, int_min()));
+      case Intr::Addc: {
+        // ahi + bhi + ltu(alo + blo, alo), with ltu spelled out as above
+        Expr lo = binary(Bin::Add, c.a[2], c.a[3]);
+        Expr carry = binary(Bin::Lt, binary(Bin::Xor, lo, int_min()), binary(Bin::Xor, c.a[2], int_min()));
+        return binary(Bin::Add, binary(Bin::Add, c.a[0], c.a[1]), carry);
+      }
       case Intr::Fshr:
       case Intr::Fshl: {
         // fshr(lo, hi, n) = n&31 == 0 ? lo : shr_u(lo, n) | hi << (32 - n)

@@ -287,9 +287,10 @@ class Lane:
 
 
 def add64(src, a, b):
-    src(f"t = {a.lo} + {b.lo};")
-    src(f"{a.hi} = {a.hi} + {b.hi} + ltu(t, {a.lo});")
-    src(f"{a.lo} = t;")
+    """a += b on 32-bit halves: the high word through MK+ addc (add.cc + addc on the B200:
+    IADD3 + IADD3.X instead of an unsigned compare and a select), then the low word."""
+    src(f"{a.hi} = addc({a.hi}, {b.hi}, {a.lo}, {b.lo});")
+    src(f"{a.lo} = {a.lo} + {b.lo};")
 
 
 def add64_m(src, a, m):
@@ -297,9 +298,8 @@ def add64_m(src, a, m):
     lo, hi = m
     if lo == "0" and hi == "0":
         return
-    src(f"t = {a.lo} + {lo};")
-    src(f"{a.hi} = {a.hi} + {hi} + ltu(t, {a.lo});")
-    src(f"{a.lo} = t;")
+    src(f"{a.hi} = addc({a.hi}, {hi}, {a.lo}, {lo});")
+    src(f"{a.lo} = {a.lo} + {lo};")
 
 
 def xor64(src, a, b):
@@ -326,7 +326,7 @@ def gen_blake2b():
     header(s, p, "blake2b", """// BLAKE2b-512 nonce search (ccminer blake2b analogue, PAPER.md:876).
 // Generated by kernels/gen_crypto.py. Message = 80-byte header of little-endian words
 // (scalar params h0..h18, word 19 = nonce): one compression with t = 80 and the final flag.
-// 64-bit lanes live in 32-bit halves: adds carry through ltu, rotates are funnel shifts
+// 64-bit lanes live in 32-bit halves: adds carry through addc (add.cc/addc), rotates are funnel shifts
 // (SHF on sm_100a) and rotations by 32 are free renames. Criterion/checksum word = the low
 // 32 bits of digest lane 0.""",
            f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], {hp}, int {p}_nonce0, int {p}_count, int {p}_target",

@@ -195,3 +195,30 @@ def test_warp_bcast_lowering_on_reference_interpreter(hf, tmp_path):
     with pytest.raises(hf.HFuseError) as e:
         hf.check(BCAST.replace("(g + 3) % 8, 8)", "(g + 3) % 8, 6)"))
     assert "power of two" in e.value.message
+
+
+ADDC = """kernel k(int al[], int ah[], int bl[], int bh[], int ol[], int oh[]) dims (64, 1, 1) {
+  int t = threadIdx.x;
+  oh[t] = addc(ah[t], bh[t], al[t], bl[t]);
+  ol[t] = al[t] + bl[t];
+}
+"""
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_addc_is_the_high_word_of_a_64_bit_add(hf, tmp_path):
+    """MK+ addc(ahi, bhi, alo, blo): lowered (ltu carry) on the reference interpreter it equals
+    the high word of the 64-bit sum; the sm_100a emission is add.cc + addc."""
+    import numpy as np
+    img = "".join(f"array {n} int32 64 seed {i + 3} range -2147483648 2147483647\n"
+                  for i, n in enumerate(["al", "ah", "bl", "bh"])) + "array ol int32 64 zero\narray oh int32 64 zero\n"
+    (tmp_path / "k.mk").write_text(hf.lower(ADDC))
+    (tmp_path / "k.img").write_text(img)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img")
+    out, _ = oracle.parse_image(dump)
+    x, _ = oracle.parse_image(img)
+    u = {k: np.asarray(x[k], np.int64) & 0xFFFFFFFF for k in ("al", "ah", "bl", "bh")}
+    s = ((u["ah"] << 32) | u["al"]) + ((u["bh"] << 32) | u["bl"])
+    assert np.array_equal(np.asarray(out["oh"], np.int64) & 0xFFFFFFFF, (s >> 32) & 0xFFFFFFFF)
+    assert np.array_equal(np.asarray(out["ol"], np.int64) & 0xFFFFFFFF, s & 0xFFFFFFFF)
+    assert "add.cc.u32" in hf.emit_kernel(ADDC)
