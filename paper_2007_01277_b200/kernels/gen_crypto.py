@@ -286,11 +286,30 @@ class Lane:
         self.lo, self.hi = lo, hi
 
 
+# How 64-bit adds carry (BLAKE2b): "ltu" = unsigned compare + select (ISETP + IMAD: the select
+# runs on the FMA pipe), "addc" = MK+ addc (add.cc/addc: IADD3 + IADD3.X, fewer instructions but
+# all on the ALU pipe), "mix" = alternate. See profiles/r01_probe_blake2b_carry.json.
+ADD64 = os.environ.get("HF_ADD64", "ltu")
+_add64_n = [0]
+
+
+def _use_addc():
+    _add64_n[0] += 1
+    return ADD64 == "addc" or (ADD64 == "mix" and _add64_n[0] % 2 == 0)
+
+
+def _add64(src, a, hi_b, lo_b):
+    if _use_addc():
+        src(f"{a.hi} = addc({a.hi}, {hi_b}, {a.lo}, {lo_b});")
+        src(f"{a.lo} = {a.lo} + {lo_b};")
+    else:
+        src(f"t = {a.lo} + {lo_b};")
+        src(f"{a.hi} = {a.hi} + {hi_b} + ltu(t, {a.lo});")
+        src(f"{a.lo} = t;")
+
+
 def add64(src, a, b):
-    """a += b on 32-bit halves: the high word through MK+ addc (add.cc + addc on the B200:
-    IADD3 + IADD3.X instead of an unsigned compare and a select), then the low word."""
-    src(f"{a.hi} = addc({a.hi}, {b.hi}, {a.lo}, {b.lo});")
-    src(f"{a.lo} = {a.lo} + {b.lo};")
+    _add64(src, a, b.hi, b.lo)
 
 
 def add64_m(src, a, m):
@@ -298,8 +317,7 @@ def add64_m(src, a, m):
     lo, hi = m
     if lo == "0" and hi == "0":
         return
-    src(f"{a.hi} = addc({a.hi}, {hi}, {a.lo}, {lo});")
-    src(f"{a.lo} = {a.lo} + {lo};")
+    _add64(src, a, hi, lo)
 
 
 def xor64(src, a, b):
@@ -326,7 +344,7 @@ def gen_blake2b():
     header(s, p, "blake2b", """// BLAKE2b-512 nonce search (ccminer blake2b analogue, PAPER.md:876).
 // Generated by kernels/gen_crypto.py. Message = 80-byte header of little-endian words
 // (scalar params h0..h18, word 19 = nonce): one compression with t = 80 and the final flag.
-// 64-bit lanes live in 32-bit halves: adds carry through addc (add.cc/addc), rotates are funnel shifts
+// 64-bit lanes live in 32-bit halves: adds carry through """ + ("ltu (compare + select)" if ADD64 == "ltu" else "addc (add.cc/addc)" if ADD64 == "addc" else "alternately ltu and addc") + """, rotates are funnel shifts
 // (SHF on sm_100a) and rotations by 32 are free renames. Criterion/checksum word = the low
 // 32 bits of digest lane 0.""",
            f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], {hp}, int {p}_nonce0, int {p}_count, int {p}_target",
