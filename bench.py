@@ -272,6 +272,7 @@ def main():
     ap.add_argument("--grids", default="296,592,1184,2368",
                     help="launch grids tried for every DL member and fused pair (multiples of 148 SMs)")
     ap.add_argument("--search-reps", type=int, default=5)
+    ap.add_argument("--d0s", default="1024,512", help="fused block sizes searched for the DL pairs")
     ap.add_argument("--granularity", type=int, default=64,
                     help="split step of the partition sweep (the reference sweeps 128)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -311,6 +312,7 @@ def main():
     keys = sorted({k for p in pair_list for k in p})
     grids = [int(g) for g in args.grids.split(",")] if args.grids else [args.grid]
     flush = args.l2 == "flush"
+    d0s = [int(x) for x in args.d0s.split(",")]
     stream = torch.cuda.current_stream()
 
     # ---- setup: one image holding every member's arrays (bound by name), per-rank shard seed
@@ -340,13 +342,15 @@ def main():
     t_setup = time.perf_counter()
     for a, b in pair_list:
         r, grid, trace = None, None, []
-        for g in grids:
-            rg = hf.search(src[a], src[b], img, d0=1024, grid=g, reps=args.search_reps, warmup=2, specialize=True,
-                           flush_l2=flush,
-                           granularity=args.granularity)
-            trace += [(g, t["d1"], t["reg_cap"], round(t["us"], 2)) for t in rg["trace"]]
-            if r is None or rg["best_time"] < r["best_time"]:
-                r, grid = rg, g
+        # fused block sizes: 1024 threads (2 blocks / SM) and 512 (4 blocks / SM, twice the
+        # grid), each with every split at the search granularity
+        for d0 in d0s:
+            for g in grids if d0 == 1024 else [2 * x for x in grids]:
+                rg = hf.search(src[a], src[b], img, d0=d0, grid=g, reps=args.search_reps, warmup=2,
+                               specialize=True, flush_l2=flush, granularity=args.granularity)
+                trace += [(d0, g, t["d1"], t["reg_cap"], round(t["us"], 2)) for t in rg["trace"]]
+                if r is None or rg["best_time"] < r["best_time"]:
+                    r, grid = rg, g
         cap = r["reg_cap"]
         m = hf.Module.fused(src[a], src[b], r["d1"], r["d2"], regcap=cap if cap else "off", grid=grid,
                             specialize=img)
@@ -369,7 +373,8 @@ def main():
         vert = hf.Module.vertical(src[a], src[b], grid, specialize=img)
         tv = min(hf.time("single", vert, None, img, g, warmup=2, reps=10, flush_l2=flush, stream=stream)["iqm_us"]
                  for g in grids)
-        results.append({"pair": f"{a}+{b}", "grid": grid, "d1": r["d1"], "d2": r["d2"], "reg_cap": cap,
+        results.append({"pair": f"{a}+{b}", "grid": grid, "d0": r["d1"] + r["d2"], "d1": r["d1"], "d2": r["d2"],
+                        "reg_cap": cap,
                         "grid_a": ga, "grid_b": gb,
                         "bytes": work[a].bytes + work[b].bytes, "regs": m.info.regs,
                         "blocks_per_sm": m.info.blocks_per_sm, "fused_us": fz["iqm_us"],
@@ -513,7 +518,7 @@ def main():
         "data": "synthetic (splitmix64-seeded in HBM; per-rank shard seed)",
         "config": {"workload": "C2: all 10 DL pairs of {BatchNorm-stats 64x256x56x56, Hist 64x256x56x56, "
                                "Im2Col 32x64x56x56, MaxPool 64x64x112x112, Upsample 64x256x28x28} fused at the "
-                               "searched best (grid, split, register cap) at d0=1024", "grids": grids,
+                               "searched best (block size d0 in {1024, 512}, grid, split, register cap)", "grids": grids,
                    "pairs": len(results), "member_grid_us": member_sweep,
                    "l2": ("step: inputs per pair >= 410 MB > 126 MB L2, no flush; per-pair tables: "
                           + ("back-to-back repetitions (each pays the previous one's write-back)" if not flush
