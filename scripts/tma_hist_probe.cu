@@ -79,6 +79,71 @@ __global__ void __launch_bounds__(1024) hist_tma(const float* __restrict__ x, in
   }
 }
 
+
+// (c) warp-specialized: warp 0 lane 0 produces (waits on empty[s], issues the bulk copy into
+// stage s, full[s] completes on the bytes); the other warps consume (wait full[s], bin their
+// share, one arrive per warp on empty[s]) -- no block barrier in the loop
+template <int STAGES, int CHUNK>
+__global__ void __launch_bounds__(1024) hist_tma_ws(const float* __restrict__ x, int n, int* out) {
+  extern __shared__ __align__(128) char buf[];
+  __shared__ int bins[2048];
+  __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES];
+  const int nwarps = blockDim.x / 32, cw = nwarps - 1;  // consumer warps
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) bins[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&full[s])));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&empty[s])), "r"(cw));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  const int per = CHUNK / 4, chunks = n / per, wb = (threadIdx.x / 32) * 64;
+  auto wait = [](unsigned long long* bar, unsigned parity) {
+    unsigned done = 0, b = (unsigned)__cvta_generic_to_shared(bar);
+    while (!done)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(done) : "r"(b), "r"(parity));
+  };
+  if (threadIdx.x < 32) {  // producer warp
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (int c = blockIdx.x; c < chunks; c += gridDim.x, ++k) {
+        int s = k % STAGES;
+        if (k >= STAGES) wait(&empty[s], ((k / STAGES) - 1) & 1);
+        unsigned b = (unsigned)__cvta_generic_to_shared(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(b), "r"(CHUNK));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(buf + s * CHUNK)),
+                     "l"(x + size_t(c) * per), "r"(CHUNK), "r"(b)
+                     : "memory");
+      }
+    }
+  } else {  // consumer warps
+    const int ct = threadIdx.x - 32;
+    int k = 0;
+    for (int c = blockIdx.x; c < chunks; c += gridDim.x, ++k) {
+      int s = k % STAGES;
+      wait(&full[s], (k / STAGES) & 1);
+      const float4* v = reinterpret_cast<const float4*>(buf + s * CHUNK);
+      for (int i = ct; i < CHUNK / 16; i += cw * 32) {
+        float4 q = v[i];
+        bin(bins, wb, q.x); bin(bins, wb, q.y); bin(bins, wb, q.z); bin(bins, wb, q.w);
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0)
+        asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&empty[s])));
+    }
+  }
+  for (int i = chunks * per + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) bin(bins, wb, x[i]);
+  __syncthreads();
+  for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+    int t = 0;
+    for (int w = 0; w < blockDim.x / 32; ++w) t += bins[w * 64 + b];
+    atomicAdd(&out[b], t);
+  }
+}
+
 __global__ void fill(float* x, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     unsigned h = i * 2654435761u;
@@ -92,7 +157,7 @@ int main() {
   float* x;
   int* out;
   cudaMalloc(&x, size_t(n) * 4);
-  cudaMalloc(&out, 64 * 4 * 8);
+  cudaMalloc(&out, 64 * 4 * 8);  // 7 result slots used
   fill<<<1184, 256>>>(x, n);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -127,6 +192,13 @@ int main() {
   run("tma_4x16KB", 2 * sms, [&] { hist_tma<S4, C16><<<2 * sms, 1024, S4 * C16>>>(x, n, out + 64); }, 1);
   run("tma_3x32KB", 2 * sms, [&] { hist_tma<S3, C32><<<2 * sms, 1024, S3 * C32>>>(x, n, out + 128); }, 2);
   run("tma_4x16KB_g1", sms, [&] { hist_tma<S4, C16><<<sms, 1024, S4 * C16>>>(x, n, out + 192); }, 3);
+  constexpr int S6 = 6, S8 = 8, C8 = 8192;
+  cudaFuncSetAttribute(hist_tma_ws<S4, C16>, cudaFuncAttributeMaxDynamicSharedMemorySize, S4 * C16);
+  cudaFuncSetAttribute(hist_tma_ws<S6, C16>, cudaFuncAttributeMaxDynamicSharedMemorySize, S6 * C16);
+  cudaFuncSetAttribute(hist_tma_ws<S8, C8>, cudaFuncAttributeMaxDynamicSharedMemorySize, S8 * C8);
+  run("ws_4x16KB", 2 * sms, [&] { hist_tma_ws<S4, C16><<<2 * sms, 1024, S4 * C16>>>(x, n, out + 256); }, 4);
+  run("ws_6x16KB", 2 * sms, [&] { hist_tma_ws<S6, C16><<<2 * sms, 1024, S6 * C16>>>(x, n, out + 320); }, 5);
+  run("ws_8x8KB", 2 * sms, [&] { hist_tma_ws<S8, C8><<<2 * sms, 1024, S8 * C8>>>(x, n, out + 384); }, 6);
   std::printf("{}]\n");
   return 0;
 }
