@@ -29,7 +29,7 @@ if args.from_bench:
     if args.only_pairs:
         rows = [r for r in rows if r["pair"] in args.only_pairs.split(",")]
         keys = []
-    pairs = [(r["pair"], r["d1"], r["grid"], r["reg_cap"]) for r in rows]
+    pairs = [(r["pair"], r["d1"], r["grid"], r["reg_cap"], r["d2"]) for r in rows]
     mgrid = {}
     for r in bench["pairs"]:
         a, b = r["pair"].split("+")
@@ -46,8 +46,9 @@ for p in pairs:
     a, b = p[0].split("+")
     g = int(p[2]) if len(p) > 2 else args.grid
     cap = p[3] if len(p) > 3 and p[3] else "off"
+    d2 = int(p[4]) if len(p) > 4 else 1024 - int(p[1])
     m = hf.Module.fused(P.source(args.form, P.MEMBERS[a].stem), P.source(args.form, P.MEMBERS[b].stem),
-                        int(p[1]), 1024 - int(p[1]), regcap=cap, grid=g, specialize=img)
+                        int(p[1]), d2, regcap=cap, grid=g, specialize=img)
     m.run(img, g)
 import ctypes  # noqa: E402
 ctypes.CDLL("libcudart.so.12").cudaDeviceSynchronize()
