@@ -358,10 +358,10 @@ def main():
         pgrid[(a, b)] = grid
         ga, gb = mgrid[a], mgrid[b]
         # one protocol for all variants: L2 flushed (clean) before every repetition
-        fz = hf.time("single", m, None, img, grid, warmup=2, reps=30, flush_l2=flush, stream=stream)
-        seq = hf.time("sequential", unfused[a], unfused[b], img, ga, gb, warmup=2, reps=30, flush_l2=flush,
+        fz = hf.time("single", m, None, img, grid, warmup=5, reps=60, flush_l2=flush, stream=stream)
+        seq = hf.time("sequential", unfused[a], unfused[b], img, ga, gb, warmup=5, reps=60, flush_l2=flush,
                       stream=stream)
-        two = hf.time("two_stream", unfused[a], unfused[b], img, ga, gb, warmup=2, reps=30, flush_l2=flush,
+        two = hf.time("two_stream", unfused[a], unfused[b], img, ga, gb, warmup=5, reps=60, flush_l2=flush,
                       stream=stream)
         ta = hf.time("single", unfused[a], None, img, ga, warmup=2, reps=10, flush_l2=flush, stream=stream)
         tb = hf.time("single", unfused[b], None, img, gb, warmup=2, reps=10, flush_l2=flush, stream=stream)
