@@ -220,3 +220,26 @@ def test_requires_violation_fails_loudly_on_device(gpu):
     assert e.value.name == "InvalidArgument" and "bn_HW % 4 == 0" in str(e.value) and "bn_HW = 18" in str(e.value)
     good = hf.Image(pairs._bn(2, 3, 16)(0).image).upload()
     mod.run(good, 4)
+
+
+@pytest.mark.gpu
+def test_preexisting_named_barriers_synchronize_their_own_interval(gpu):
+    """SURVEY App. C on the device: both constituents hand data across bar_sync(1, 64) in shared
+    memory; fused, each gets its own barrier id (the reference would let them share id 1), so
+    every thread reads its neighbour's value, over 64 blocks and 20 launches."""
+    hf = gpu
+    k1 = ("kernel a(int x[]) dims (64, 1, 1) {\n  shared int s[64];\n  int t = threadIdx.x;\n"
+          "  s[t] = t * 3 + blockIdx.x;\n  bar_sync(1, 64);\n  x[blockIdx.x * 64 + t] = s[(t + 1) % 64];\n}\n")
+    k2 = ("kernel b(int y[]) dims (64, 1, 1) {\n  shared int r[64];\n  int t = threadIdx.x;\n"
+          "  r[t] = t * 7 - blockIdx.x;\n  bar_sync(1, 64);\n  y[blockIdx.x * 64 + t] = r[(t + 63) % 64];\n}\n")
+    m = hf.Module.fused(k1, k2, 64, 64, grid=64)
+    ids = {(b.owner, b.original): b.id for b in m.barriers}
+    assert ids[(1, 1)] != ids[(2, 1)]
+    img = hf.Image("array x int32 4096 zero\narray y int32 4096 zero\n").upload()
+    t = np.arange(64)
+    want_x = np.concatenate([((t + 1) % 64) * 3 + b for b in range(64)])
+    want_y = np.concatenate([((t + 63) % 64) * 7 - b for b in range(64)])
+    for _ in range(20):
+        m.run(img, 64)
+        img.download()
+        assert np.array_equal(img.array("x"), want_x) and np.array_equal(img.array("y"), want_y)
