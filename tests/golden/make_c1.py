@@ -1,0 +1,42 @@
+"""C1 at full size on the UNMODIFIED reference interpreter (TEST INFRASTRUCTURE; BASELINE
+configs[0]: BatchNorm-collect-stats + Hist on a 64x256x56x56 fp32 tensor, equivalence check).
+The B200 member forms, lowered to plain Mini-Kernel (hfuse lower), run sequentially at the split
+d1/d2 and grid G the GPU test fuses them with (run_functional, acceptance_main.cpp:147-152); the
+fused sm_100a kernel must reproduce the resulting FNV-1a digest over all arrays bit for bit.
+Writes c1_full.json (digest, split, grid, the interpreter's wall time)."""
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.abspath(os.path.join(HERE, "..", ".."))
+sys.path.insert(0, ROOT)
+
+from oracle import oracle  # noqa: E402
+from paper_2007_01277_b200 import hfuse as hf  # noqa: E402
+from paper_2007_01277_b200 import pairs  # noqa: E402
+
+D1, D2, GRID = 512, 512, 296
+
+
+def main():
+    with tempfile.TemporaryDirectory() as d:
+        k1, k2, img = (os.path.join(d, n) for n in ("bn.mk", "hist.mk", "c1.img"))
+        open(k1, "w").write(hf.lower(pairs.source("b200", "batchnorm")))
+        open(k2, "w").write(hf.lower(pairs.source("b200", "histogram")))
+        open(img, "w").write(pairs.MEMBERS["bn"].sizes["full"](0).image + pairs.MEMBERS["hist"].sizes["full"](0).image)
+        r = subprocess.run([oracle.REF, "seq", k1, k2, "--d1", str(D1), "--d2", str(D2), "--mem", img, "--grid",
+                            str(GRID), "--time"], capture_output=True, text=True, timeout=3600)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr)
+        kv = dict(line.split(" = ") for line in r.stdout.strip().splitlines())
+    out = {"pair": "bn+hist", "form": "b200 (lowered)", "d1": D1, "d2": D2, "grid": GRID,
+           "digest": kv["digest"], "interpreter_seconds": float(kv["seconds"])}
+    json.dump(out, open(os.path.join(HERE, "c1_full.json"), "w"), indent=1)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -243,3 +243,19 @@ def test_preexisting_named_barriers_synchronize_their_own_interval(gpu):
         m.run(img, 64)
         img.download()
         assert np.array_equal(img.array("x"), want_x) and np.array_equal(img.array("y"), want_y)
+
+
+@pytest.mark.gpu
+def test_c1_full_size_equals_reference_interpreter(gpu):
+    """BASELINE configs[0] on the device: the fused BatchNorm-stats + Hist kernel over the
+    64x256x56x56 tensors (2 x 205.5 MB) reproduces the reference interpreter's sequential run of
+    the same (lowered) member forms bit for bit (tests/golden/make_c1.py, ~9 s of CPU)."""
+    hf = gpu
+    ref = golden("c1_full.json")
+    img = hf.Image(pairs.MEMBERS["bn"].sizes["full"](0).image).merge(
+        hf.Image(pairs.MEMBERS["hist"].sizes["full"](0).image)).upload()
+    m = hf.Module.fused(pairs.source("b200", "batchnorm"), pairs.source("b200", "histogram"), ref["d1"], ref["d2"],
+                        grid=ref["grid"], specialize=img)
+    m.run(img, ref["grid"])
+    img.download()
+    assert img.digest_hex() == ref["digest"]
