@@ -259,3 +259,23 @@ def test_c1_full_size_equals_reference_interpreter(gpu):
     m.run(img, ref["grid"])
     img.download()
     assert img.digest_hex() == ref["digest"]
+
+
+FULL = golden("full_pairs.json")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pair", list(FULL))
+def test_full_size_pair_equals_reference_interpreter(gpu, pair):
+    """Every DL pair at its C2 size (hundreds of MB): the fused kernel equals the reference
+    interpreter's sequential run of the lowered members at the same split and grid, bit for bit."""
+    hf = gpu
+    ref = FULL[pair]
+    a, b = pair.split("+")
+    img = hf.Image(pairs.MEMBERS[a].sizes["full"](0).image).merge(
+        hf.Image(pairs.MEMBERS[b].sizes["full"](0).image)).upload()
+    m = hf.Module.fused(pairs.source("b200", pairs.MEMBERS[a].stem), pairs.source("b200", pairs.MEMBERS[b].stem),
+                        ref["d1"], ref["d2"], grid=ref["grid"], specialize=img)
+    m.run(img, ref["grid"])
+    img.download()
+    assert img.digest_hex() == ref["digest"]
