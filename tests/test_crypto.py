@@ -130,3 +130,19 @@ def test_fused_crypto_pairs_with_interval_budgets(gpu, a, b, d2, regs):
     img.download()
     assert device_outputs(img, a) == reference_outputs(a, ca, grid, 5, 1 << 28)
     assert device_outputs(img, b) == reference_outputs(b, cb, grid, 9, 1 << 28, threads=d2)
+
+
+@pytest.mark.gpu
+def test_sha256d_blake2b_fused_at_scale(gpu):
+    """2^20 nonces of each member through the fused kernel at the bench's grid (296) equals the
+    hashlib-based restatement: hit count, checksum and every block's minimum winning nonce."""
+    hf = gpu
+    grid, n = 296, 1 << 20
+    wa = crypto.workload("sha256d", count=n, grid=grid, nonce0=123, target=1 << 20)
+    wb = crypto.workload("blake2b", count=n, grid=grid, nonce0=456, target=1 << 20)
+    img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
+    m = hf.Module.fused(src("sha256d"), src("blake2b"), 512, 512, grid=grid, specialize=img)
+    m.run(img, grid)
+    img.download()
+    assert device_outputs(img, "sha256d") == reference_outputs("sha256d", n, grid, 123, 1 << 20)
+    assert device_outputs(img, "blake2b") == reference_outputs("blake2b", n, grid, 456, 1 << 20)
