@@ -213,6 +213,13 @@ int hf_module_cubin(const hf_module* m, const void** data, size_t* size);
 /* Raw launch: args[i] points at the i-th parameter value (device pointer or scalar);
  * specialized scalars are checked against the folded value. */
 int hf_launch(const hf_module* m, int grid, void** args, void* stream, hf_error* err);
+/* hf_launch / hf_run with flags. HF_LAUNCH_OVERLAP: programmatic dependent launch -- the kernel
+ * may start while the previous kernel in the stream drains (every emitted kernel triggers
+ * griddepcontrol.launch_dependents on entry). Only for a kernel that does not read what the
+ * previous one writes (independent fused pairs in a step); B200-only, no reference analogue. */
+enum { HF_LAUNCH_OVERLAP = 1 };
+int hf_launch_ex(const hf_module* m, int grid, void** args, void* stream, int flags, hf_error* err);
+int hf_run_ex(const hf_module* m, hf_image* img, int grid, void* stream, int flags, hf_error* err);
 void hf_module_free(hf_module* m);
 
 /* MemoryImage (memimage.hpp:36-68); seeded arrays are generated in HBM on upload. */

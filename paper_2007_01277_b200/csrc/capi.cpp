@@ -306,6 +306,10 @@ int hf_module_cubin(const hf_module* m, const void** data, size_t* size) {
 }
 
 int hf_launch(const hf_module* m, int grid, void** args, void* stream, hf_error* err) {
+  return hf_launch_ex(m, grid, args, stream, 0, err);
+}
+
+int hf_launch_ex(const hf_module* m, int grid, void** args, void* stream, int flags, hf_error* err) {
   return guarded(err, [&] {
     for (size_t i = 0; i < m->m.params.size(); ++i) {
       const auto& p = m->m.params[i];
@@ -316,7 +320,7 @@ int hf_launch(const hf_module* m, int grid, void** args, void* stream, hf_error*
         hf::raise(hf::Code::InvalidArgument, "module is specialized for a different value of scalar '" + p.name + "'");
     }
     hf::rt::check_requires(m->m, args);
-    hf::rt::launch_raw(m->m, grid > 0 ? grid : m->m.grid, args, stream);
+    hf::rt::launch_raw(m->m, grid > 0 ? grid : m->m.grid, args, stream, (flags & HF_LAUNCH_OVERLAP) != 0);
   });
 }
 
@@ -409,7 +413,11 @@ void hf_image_free(hf_image* img) {
 }
 
 int hf_run(const hf_module* m, hf_image* img, int grid, void* stream, hf_error* err) {
-  return guarded(err, [&] { hf::rt::launch(m->m, img->img, grid, stream); });
+  return hf_run_ex(m, img, grid, stream, 0, err);
+}
+
+int hf_run_ex(const hf_module* m, hf_image* img, int grid, void* stream, int flags, hf_error* err) {
+  return guarded(err, [&] { hf::rt::launch(m->m, img->img, grid, stream, (flags & HF_LAUNCH_OVERLAP) != 0); });
 }
 
 int hf_time(int mode, const hf_module* a, const hf_module* b, hf_image* img, int grid_a, int grid_b, int warmup,

@@ -39,6 +39,7 @@ struct Driver {
   CUresult (*moduleUnload)(CUmodule) = nullptr;
   CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void**, void**) = nullptr;
+  CUresult (*launchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
   CUresult (*funcGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
   CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
@@ -65,6 +66,7 @@ Driver& drv() {
     resolve("cuModuleGetFunction", d.moduleGetFunction);
     resolve("cuModuleUnload", d.moduleUnload);
     resolve("cuLaunchKernel", d.launchKernel);
+    resolve("cuLaunchKernelEx", d.launchKernelEx);
     resolve("cuFuncGetAttribute", d.funcGetAttribute);
     resolve("cuFuncSetAttribute", d.funcSetAttribute);
     resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy);
@@ -435,11 +437,30 @@ void* device_ptr(Image& img, const std::string& name) {
   return it->second.dev;
 }
 
-void launch_raw(const Module& m, int grid, void** args, void* stream) {
+void launch_raw(const Module& m, int grid, void** args, void* stream, bool overlap) {
   if (!m.fn) raise(Code::Device, "module '" + m.entry + "' is not loaded (no GPU?)");
-  cu_check(drv().launchKernel(static_cast<CUfunction>(m.fn), unsigned(grid), 1, 1, unsigned(m.threads), 1, 1,
-                              unsigned(m.smem), static_cast<CUstream>(stream), args, nullptr),
-           "cuLaunchKernel");
+  if (!overlap) {
+    cu_check(drv().launchKernel(static_cast<CUfunction>(m.fn), unsigned(grid), 1, 1, unsigned(m.threads), 1, 1,
+                                unsigned(m.smem), static_cast<CUstream>(stream), args, nullptr),
+             "cuLaunchKernel");
+    return;
+  }
+  // programmatic dependent launch: this grid may start while the previous kernel of the stream
+  // drains (every emitted kernel triggers griddepcontrol.launch_dependents on entry); the caller
+  // asserts that this kernel does not read what that one writes
+  CUlaunchAttribute attr{};
+  attr.id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  attr.value.programmaticStreamSerializationAllowed = 1;
+  CUlaunchConfig cfg{};
+  cfg.gridDimX = unsigned(grid);
+  cfg.gridDimY = cfg.gridDimZ = 1;
+  cfg.blockDimX = unsigned(m.threads);
+  cfg.blockDimY = cfg.blockDimZ = 1;
+  cfg.sharedMemBytes = unsigned(m.smem);
+  cfg.hStream = static_cast<CUstream>(stream);
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  cu_check(drv().launchKernelEx(&cfg, static_cast<CUfunction>(m.fn), args, nullptr), "cuLaunchKernelEx");
 }
 
 void check_requires(const Module& m, void* const* args) {
@@ -507,9 +528,9 @@ Bound bind(const Module& m, Image& img) {
 }
 }  // namespace
 
-void launch(const Module& m, Image& img, int grid, void* stream) {
+void launch(const Module& m, Image& img, int grid, void* stream, bool overlap) {
   Bound b = bind(m, img);
-  launch_raw(m, grid > 0 ? grid : m.grid, b.args.data(), stream);
+  launch_raw(m, grid > 0 ? grid : m.grid, b.args.data(), stream, overlap);
 }
 
 Timing time(Mode mode, const Module& a, const Module* b, Image& img, int grid_a, int grid_b, int warmup, int reps,

@@ -64,8 +64,10 @@ void release(Image& img);
 void* device_ptr(Image& img, const std::string& name);
 
 // Binds parameters by name from the image (exec.cpp:190-216) and launches.
-void launch(const Module& m, Image& img, int grid, void* stream = nullptr);
-void launch_raw(const Module& m, int grid, void** args, void* stream = nullptr);
+// overlap: programmatic dependent launch (the kernel may start while the stream's previous kernel
+// drains; only for kernels that do not read what that kernel writes)
+void launch(const Module& m, Image& img, int grid, void* stream = nullptr, bool overlap = false);
+void launch_raw(const Module& m, int grid, void** args, void* stream = nullptr, bool overlap = false);
 // Throws InvalidArgument when a `//@ requires` precondition is false for these scalar values
 // (args[i] points at parameter i's value; specialized parameters use their folded value).
 void check_requires(const Module& m, void* const* args);

@@ -41,7 +41,7 @@ EXPORTS = [
     "hf_get_device_props", "hf_build_fused", "hf_build_fused_regs", "hf_build_kernel", "hf_build_naive", "hf_build_vertical",
     "hf_module_get_info",
     "hf_module_source", "hf_module_entry", "hf_module_param", "hf_module_param_reads", "hf_module_barrier",
-    "hf_module_cubin", "hf_launch", "hf_module_free", "hf_image_parse", "hf_image_merge",
+    "hf_module_cubin", "hf_launch", "hf_launch_ex", "hf_run_ex", "hf_module_free", "hf_image_parse", "hf_image_merge",
     "hf_image_materialize", "hf_image_upload", "hf_image_download", "hf_image_digest",
     "hf_image_serialize", "hf_image_count", "hf_image_entry", "hf_image_find",
     "hf_image_set_host", "hf_image_bytes", "hf_image_free", "hf_run", "hf_time", "hf_profile",
@@ -138,6 +138,8 @@ def _load() -> C.CDLL:
         "hf_module_barrier": (ip, [vp, ip, C.POINTER(_Barrier)]),
         "hf_module_cubin": (ip, [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]),
         "hf_launch": (ip, [vp, ip, C.POINTER(vp), vp, E]),
+        "hf_launch_ex": (ip, [vp, ip, C.POINTER(vp), vp, ip, E]),
+        "hf_run_ex": (ip, [vp, vp, ip, vp, ip, E]),
         "hf_module_free": (None, [vp]),
         "hf_image_parse": (ip, [cp, ip, C.c_ulonglong, C.POINTER(vp), E]),
         "hf_image_merge": (ip, [vp, vp, E]),
@@ -486,11 +488,13 @@ class Module:
         _lib.hf_module_cubin(self._h, C.byref(p), C.byref(n))
         return C.string_at(p, n.value)
 
-    def run(self, img: Image, grid: int = 0, stream=None) -> None:
+    def run(self, img: Image, grid: int = 0, stream=None, overlap: bool = False) -> None:
+        """overlap: programmatic dependent launch (HF_LAUNCH_OVERLAP) -- may start while the
+        previous kernel of the stream drains; only for kernels independent of that one."""
         err = _Err()
-        _check(_lib.hf_run(self._h, img._h, grid, _stream(stream), C.byref(err)), err)
+        _check(_lib.hf_run_ex(self._h, img._h, grid, _stream(stream), int(overlap), C.byref(err)), err)
 
-    def launch(self, args: Dict[str, object], grid: int = 0, stream=None) -> None:
+    def launch(self, args: Dict[str, object], grid: int = 0, stream=None, overlap: bool = False) -> None:
         """Raw launch: args maps parameter name -> device pointer (int / torch tensor) or scalar."""
         keep, ptrs = [], []
         for p in self.params:
@@ -505,7 +509,7 @@ class Module:
             ptrs.append(C.cast(C.pointer(cell), C.c_void_p))
         arr = (C.c_void_p * len(ptrs))(*ptrs)
         err = _Err()
-        _check(_lib.hf_launch(self._h, grid, arr, _stream(stream), C.byref(err)), err)
+        _check(_lib.hf_launch_ex(self._h, grid, arr, _stream(stream), int(overlap), C.byref(err)), err)
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -279,3 +279,22 @@ def test_full_size_pair_equals_reference_interpreter(gpu, pair):
     m.run(img, ref["grid"])
     img.download()
     assert img.digest_hex() == ref["digest"]
+
+
+@pytest.mark.gpu
+def test_overlapped_launches_of_independent_pairs_match_serial(gpu):
+    """Programmatic dependent launch (HF_LAUNCH_OVERLAP) of the ten fused pairs back to back on one
+    stream -- each may start while its predecessor drains -- leaves the image exactly as ordinary
+    serialized launches do (the pairs share only identical outputs and commutative atomics)."""
+    hf = gpu
+    mods = [hf.Module.fused(pairs.source("b200", pairs.MEMBERS[a].stem), pairs.source("b200", pairs.MEMBERS[b].stem),
+                            512, 512, grid=GRID) for a, b in pairs.PAIRS]
+    digests = []
+    for overlap in (False, True):
+        img = image(hf, *pairs.ORDER).upload()
+        for _ in range(3):
+            for m in mods:
+                m.run(img, GRID, overlap=overlap)
+        img.download()
+        digests.append(img.digest_hex())
+    assert digests[0] == digests[1]
