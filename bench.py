@@ -488,6 +488,12 @@ def main():
 
     # ---- e2e: the same step through the C ABI from pinned host buffers
     e2e = e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args)
+    if dist is not None:  # the job's end-to-end step ends with its slowest rank
+        t = torch.tensor([e2e["value"]], device="cuda", dtype=torch.float64)
+        all_reduce(t, "max")
+        e2e["value"] = t.item()
+        e2e["h2d_bytes_per_step"] *= world
+        e2e["d2h_bytes_per_step"] *= world
     del img  # free the DL images before the crypto suite (the Ethash DAG alone is 4 GiB)
     crypto_res = None
     clk = clocks.summary()
