@@ -458,7 +458,9 @@ def main():
             unfused_overlap_step()
         ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in pair_list] for _ in range(args.steps)]
+        torch.cuda.nvtx.range_push("step")  # ncu --nvtx --nvtx-include "step/": the launch list of `value`
         total_ms = timed(lambda s: step(overlap=True))
+        torch.cuda.nvtx.range_pop()
         serial_ms = timed(lambda s: step(ev[s]))
         unfused_ms = timed(lambda s: unfused_step())
         unfused_overlap_ms = timed(lambda s: unfused_overlap_step())
