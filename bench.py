@@ -273,6 +273,8 @@ def main():
                     help="launch grids tried for every DL member and fused pair (multiples of 148 SMs)")
     ap.add_argument("--search-reps", type=int, default=5)
     ap.add_argument("--d0s", default="1024,512", help="fused block sizes searched for the DL pairs")
+    ap.add_argument("--shapes", default="conv2", choices=["conv2", "conv3"],
+                    help="DL tensor shapes: ResNet-50 conv2_x (the C2 configuration, default) or conv3_x")
     ap.add_argument("--granularity", type=int, default=64,
                     help="split step of the partition sweep (the reference sweeps 128)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -316,11 +318,12 @@ def main():
     stream = torch.cuda.current_stream()
 
     # ---- setup: one image holding every member's arrays (bound by name), per-rank shard seed
-    img = hf.Image(P.MEMBERS[keys[0]].sizes["full"](rank).image)
+    shape = "full" if args.shapes == "conv2" else args.shapes
+    img = hf.Image(P.MEMBERS[keys[0]].sizes[shape](rank).image)
     for k in keys[1:]:
-        img.merge(hf.Image(P.MEMBERS[k].sizes["full"](rank).image))
+        img.merge(hf.Image(P.MEMBERS[k].sizes[shape](rank).image))
     img.upload(stream)
-    work = {k: P.MEMBERS[k].sizes["full"](rank) for k in keys}
+    work = {k: P.MEMBERS[k].sizes[shape](rank) for k in keys}
     src = {k: P.source("b200", P.MEMBERS[k].stem) for k in keys}
     # JIT specialization: every module folds this image's scalar shapes into its code
     unfused = {k: hf.Module.kernel(src[k], grid=grids[0], specialize=img) for k in keys}
@@ -537,11 +540,15 @@ def main():
         "vs_baseline": None,
         "dtype": "fp32/int32",
         "data": "synthetic (splitmix64-seeded in HBM; per-rank shard seed)",
-        "config": {"workload": "C2: all 10 DL pairs of {BatchNorm-stats 64x256x56x56, Hist 64x256x56x56, "
-                               "Im2Col 32x64x56x56, MaxPool 64x64x112x112, Upsample 64x256x28x28} fused at the "
-                               "searched best (block size d0 in {1024, 512}, grid, split, register cap)", "grids": grids,
+        "config": {"workload": ("C2: all 10 DL pairs of {BatchNorm-stats 64x256x56x56, Hist 64x256x56x56, "
+                                "Im2Col 32x64x56x56, MaxPool 64x64x112x112, Upsample 64x256x28x28}"
+                                if shape == "full" else
+                                "C5 shapes (ResNet-50 conv3_x): all 10 DL pairs of {BatchNorm-stats 64x512x28x28, "
+                                "Hist 64x512x28x28, Im2Col 32x128x28x28, MaxPool 64x128x56x56, Upsample 64x512x14x14}")
+                               + " fused at the searched best (block size d0 in {1024, 512}, grid, split, register cap)",
+                   "grids": grids,
                    "pairs": len(results), "member_grid_us": member_sweep,
-                   "l2": ("step: inputs per pair >= 410 MB > 126 MB L2, no flush; per-pair tables: "
+                   "l2": ("step: inputs per pair > 126 MB L2, no flush; per-pair tables: "
                           + ("back-to-back repetitions (each pays the previous one's write-back)" if not flush
                              else "read-sweep flush before every repetition")),
                    "parallelism": f"dp{world} (batch shards)"},

@@ -32,6 +32,8 @@ class Member:
     key: str
     stem: str
     sizes: Dict[str, Callable[[int], Workload]]  # size name -> f(seed offset) -> Workload
+    # "full": the C2 shapes (ResNet-50 conv2_x, 56 x 56); "conv3": ResNet-50 conv3_x shapes
+    # (28 x 28 spatial, twice the channels; bench.py --shapes conv3); parity / tiny: test sizes
 
 
 BN_SLOTS = 64  # >= grid / C + 2 for every grid the bench tries (C = 256: grids up to 15,872)
@@ -97,27 +99,32 @@ def _im2col(NC: int, H: int, W: int) -> Callable[[int], Workload]:
 MEMBERS: Dict[str, Member] = {
     "bn": Member("bn", "batchnorm", {
         "full": _bn(64, 256, 56 * 56),
+        "conv3": _bn(64, 512, 28 * 28),
         "parity": _bn(2, 8, 56 * 56),
         "tiny": _bn(1, 3, 16),
     }),
     "hist": Member("hist", "histogram", {
         "full": _hist(64 * 256 * 56 * 56),
+        "conv3": _hist(64 * 512 * 28 * 28),
         "parity": _hist(2 * 8 * 56 * 56, -4.5, 4.5),
         "tiny": _hist(64, -5.0, 5.0),
     }),
 
     "maxpool": Member("maxpool", "maxpool", {
         "full": _maxpool(64 * 64, 112, 112),
+        "conv3": _maxpool(64 * 128, 56, 56),
         "parity": _maxpool(3, 16, 16),
         "tiny": _maxpool(1, 8, 8),
     }),
     "upsample": Member("upsample", "upsample", {
         "full": _upsample(64 * 256, 28, 28),
+        "conv3": _upsample(64 * 512, 14, 14),
         "parity": _upsample(3, 8, 8),
         "tiny": _upsample(1, 4, 4),
     }),
     "im2col": Member("im2col", "im2col", {
         "full": _im2col(32 * 64, 56, 56),
+        "conv3": _im2col(32 * 128, 28, 28),
         "parity": _im2col(3, 8, 8),
         "tiny": _im2col(1, 4, 4),
     }),
