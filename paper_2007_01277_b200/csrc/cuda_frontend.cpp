@@ -19,7 +19,7 @@
 //             (MK+ vload/vstore), `make_float4(..)`, `__ldg(&a[i])`,
 //             `{ }` blocks, `__syncthreads()`, `__syncwarp()`, `__threadfence()`,
 //             `atomicAdd(&a[i], v)` as a statement, device-function calls, `#pragma unroll [N]`
-//   exprs     C operators except ?:, assignment and comma; casts (int)/(float) and int()/float();
+//   exprs     C operators (?: on integer operands, as a select) except assignment and comma; casts (int)/(float) and int()/float();
 //             min, max, fmaxf, __float2int_rz, __funnelshift_l/r, threadIdx/blockIdx/blockDim/
 //             gridDim, `__shfl_xor_sync(0xffffffff, v, m)`; float literals drop their f suffix
 // Semantics are the interpreter's: identical to CUDA for programs without
@@ -861,17 +861,31 @@ class Translator {
     return CE{"(" + l.t + " " + op + " " + r.t + ")", cmp ? 'i' : t};
   }
 
-  CE expr(int min_prec = 1) {
+  // conditional ?: on integer operands as a branch-free select (both arms are evaluated: the
+  // subset has no side effects in expressions); float arms would need a statement-level branch
+  CE expr() {
+    CE c = binexpr(1);
+    if (!is_op("?")) return c;
+    Pos p = next().pos;
+    CE a = expr();
+    want_op(":");
+    CE b = expr();
+    if (a.ty == 'f' || b.ty == 'f' || c.ty == 'f')
+      fail("?: with float operands is outside the CUDA subset (integer arms only)", p);
+    char t = (a.ty == 'u' || b.ty == 'u') ? 'u' : 'i';
+    return CE{"(" + b.t + " ^ ((" + a.t + " ^ " + b.t + ") & (0 - (" + c.t + " != 0))))", t};
+  }
+
+  CE binexpr(int min_prec) {
     CE l = unary();
     while (peek().k == CTok::Op) {
       const std::string op = peek().t;
-      if (op == "?") fail("the conditional operator ?: is outside the CUDA subset", peek().pos);
       if (op == "=" || (op.size() >= 2 && op.back() == '=' && op != "==" && op != "!=" && op != "<=" && op != ">="))
         fail("assignments inside expressions are outside the CUDA subset", peek().pos);
       int pr = prec(op);
       if (pr < min_prec || pr == 0) break;
       Pos p = next().pos;
-      CE r = expr(pr + 1);
+      CE r = binexpr(pr + 1);
       l = binary(op, l, r, p);
     }
     return l;

@@ -139,7 +139,7 @@ def test_cuda_features_lower_and_run_on_reference_interpreter(hf, tmp_path):
 
 
 @pytest.mark.parametrize("body,line,what", [
-    ("  int v = t > 0 ? 1 : 2;\n", 3, "?:"),
+    ("  float v = t > 0 ? 1.0f : 2.0f;\n", 3, "?:"),
     ("  float a[4];\n", 3, "local arrays"),
     ("  for (int i = 0; i < 4; ++i) { break; }\n", 3, "break"),
     ("  double u = 3;\n", 3, "double"),
@@ -291,3 +291,28 @@ def test_cuda_member_fused_with_mkplus_member_on_device(gpu):
     m.run(img, G["grid"])
     img.download()
     assert img.digest_hex() == G["pairs"]["bn+hist"]["512"]["digest"]
+
+
+TERNARY = r"""
+__global__ void __launch_bounds__(64) sel(const int* __restrict__ x, int* y, unsigned* z) {
+  int t = threadIdx.x;
+  int v = x[t];
+  y[t] = v > 0 ? v * 2 : (v < -100 ? -1 : v);
+  unsigned u = (unsigned)v;
+  z[t] = (t & 1) ? u : u >> 3;
+}
+"""
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_cuda_integer_conditional_as_select(hf, tmp_path):
+    """`c ? a : b` on integer operands lowers to a branch-free select (nested, unsigned arms)."""
+    img = "array x int32 64 seed 4 range -300 300\narray y int32 64 zero\narray z int32 64 zero\n"
+    (tmp_path / "k.mk").write_text(hf.lower(TERNARY))
+    (tmp_path / "k.img").write_text(img)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img")
+    out, _ = oracle.parse_image(dump)
+    x = [int(v) for v in oracle.parse_image(img)[0]["x"]]
+    assert [int(v) for v in out["y"]] == [v * 2 if v > 0 else (-1 if v < -100 else v) for v in x]
+    want_z = [(v & 0xFFFFFFFF) if t & 1 else (v & 0xFFFFFFFF) >> 3 for t, v in enumerate(x)]
+    assert [int(v) & 0xFFFFFFFF for v in out["z"]] == want_z
