@@ -17,7 +17,8 @@
 //             expression), `=` and compound assignments, `++`/`--`, if/else, for, while, return,
 //             vector loads/stores `reinterpret_cast<const float4*>(p)[i]` / `((float4*)p)[i]`
 //             (MK+ vload/vstore), `make_float4(..)`, `__ldg(&a[i])`,
-//             `{ }` blocks, `__syncthreads()`, `__syncwarp()`, `__threadfence()`,
+//             `{ }` blocks, break / continue (gotos to per-loop labels), `__syncthreads()`,
+//             `__syncwarp()`, `__threadfence()`,
 //             `atomicAdd(&a[i], v)` as a statement, device-function calls, `#pragma unroll [N]`
 //   exprs     C operators (?: on integer operands, as a select) except assignment and comma; casts (int)/(float) and int()/float();
 //             min, max, fmaxf, __float2int_rz, __funnelshift_l/r, threadIdx/blockIdx/blockDim/
@@ -423,14 +424,16 @@ class Translator {
     block_body();
   }
 
-  // `{ stmt* }` after the opening header has been emitted; emits the closing brace.
-  void block_body() {
+  // `{ stmt* }` after the opening header has been emitted; emits `before_close` (a loop's
+  // continue label) and the closing brace.
+  void block_body(const std::string& before_close = "") {
     want_op("{");
     while (!is_op("}")) {
       if (at_end()) fail("unterminated block", peek().pos);
       stmt();
     }
     Pos p = next().pos;
+    if (!before_close.empty()) put(before_close, p);
     put("}", p);
   }
 
@@ -442,6 +445,34 @@ class Translator {
     }
     stmt();
     put("}", toks_[at_ - 1].pos);
+  }
+
+  // break / continue lower to gotos to per-loop labels (Mini-Kernel labels are function-wide;
+  // emitted only when the loop uses them, so loops without either translate unchanged)
+  struct Loop {
+    int id;
+    bool brk = false, cnt = false;
+  };
+  std::vector<Loop> loops_;
+  int loop_ids_ = 0;
+
+  void loop_body(Pos p) {
+    loops_.push_back(Loop{loop_ids_++});
+    // the continue label must precede the closing brace, so the body is emitted with a
+    // placeholder that is patched once the body has been read
+    const std::string mark = "\x01cnt" + std::to_string(loops_.back().id) + "\x01";
+    if (is_op("{")) {
+      block_body(mark);
+    } else {
+      stmt();
+      put(mark, toks_[at_ - 1].pos);
+      put("}", toks_[at_ - 1].pos);
+    }
+    Loop l = loops_.back();
+    loops_.pop_back();
+    size_t at = out_.rfind(mark);
+    out_.replace(at, mark.size(), l.cnt ? "hf_cnt" + std::to_string(l.id) + ":" : "");
+    if (l.brk) put("hf_brk" + std::to_string(l.id) + ":", p);
   }
 
   void stmt() {
@@ -509,7 +540,7 @@ class Translator {
       CE c = expr();
       want_op(")");
       put("while (" + c.t + ") {", p);
-      body_stmt();
+      loop_body(p);
       return;
     }
     if (is_id("return")) {
@@ -524,7 +555,15 @@ class Translator {
       put("return " + e.t + ";", p);
       return;
     }
-    if (is_id("break") || is_id("continue") || is_id("do") || is_id("switch") || is_id("goto"))
+    if (is_id("break") || is_id("continue")) {
+      bool brk = next().t == "break";
+      want_op(";");
+      if (loops_.empty()) fail(std::string(brk ? "break" : "continue") + " outside a loop", p);
+      (brk ? loops_.back().brk : loops_.back().cnt) = true;
+      put("goto hf_" + std::string(brk ? "brk" : "cnt") + std::to_string(loops_.back().id) + ";", p);
+      return;
+    }
+    if (is_id("do") || is_id("switch") || is_id("goto"))
       fail("'" + t.t + "' is outside the CUDA subset", p);
     if (is_id("__syncthreads") || is_id("__syncwarp") || is_id("__threadfence")) {
       std::string w = next().t;
@@ -729,7 +768,7 @@ class Translator {
     std::string step = simple();
     want_op(")");
     put(unroll + "for (" + init + "; " + c.t + "; " + step + ") {", p);
-    body_stmt();
+    loop_body(p);
   }
 
   // name | name[i] | vec.c  -> (MK+ text, type)

@@ -141,7 +141,8 @@ def test_cuda_features_lower_and_run_on_reference_interpreter(hf, tmp_path):
 @pytest.mark.parametrize("body,line,what", [
     ("  float v = t > 0 ? 1.0f : 2.0f;\n", 3, "?:"),
     ("  float a[4];\n", 3, "local arrays"),
-    ("  for (int i = 0; i < 4; ++i) { break; }\n", 3, "break"),
+    ("  do { t = t + 1; } while (t < 4);\n", 3, "'do'"),
+    ("  break;\n", 3, "outside a loop"),
     ("  double u = 3;\n", 3, "double"),
     ("  unsigned u = 3u; float f = u;\n", 3, "unsigned -> float"),
     ("  unsigned u = 3u; u = u / 3u;\n", 3, "power-of-two"),
@@ -316,3 +317,60 @@ def test_cuda_integer_conditional_as_select(hf, tmp_path):
     assert [int(v) for v in out["y"]] == [v * 2 if v > 0 else (-1 if v < -100 else v) for v in x]
     want_z = [(v & 0xFFFFFFFF) if t & 1 else (v & 0xFFFFFFFF) >> 3 for t, v in enumerate(x)]
     assert [int(v) & 0xFFFFFFFF for v in out["z"]] == want_z
+
+
+LOOPS = r"""
+__global__ void __launch_bounds__(64) loops(const int* __restrict__ x, int* y) {
+  int t = threadIdx.x;
+  int acc = 0;
+  for (int i = 0; i < 16; ++i) {
+    if (i == t % 7) continue;
+    if (x[t] + i > 250) break;
+    int j = 0;
+    while (1) {
+      j++;
+      if (j > i % 3) break;
+      acc += j;
+    }
+    acc += i;
+  }
+  y[t] = acc;
+}
+"""
+
+
+def loops_reference(x):
+    out = []
+    for t, v in enumerate(x):
+        acc = 0
+        for i in range(16):
+            if i == t % 7:
+                continue
+            if v + i > 250:
+                break
+            j = 0
+            while True:
+                j += 1
+                if j > i % 3:
+                    break
+                acc += j
+            acc += i
+        out.append(acc)
+    return out
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_cuda_break_and_continue(hf, tmp_path):
+    """break / continue (nested loops) lower to gotos to per-loop labels: the reference interpreter
+    runs the translation with C's semantics, and two such kernels fuse (labels stay distinct)."""
+    img = "array x int32 64 seed 8 range 200 260\narray y int32 64 zero\n"
+    (tmp_path / "k.mk").write_text(hf.lower(LOOPS))
+    (tmp_path / "k.img").write_text(img)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img")
+    out, _ = oracle.parse_image(dump)
+    x = [int(v) for v in oracle.parse_image(img)[0]["x"]]
+    assert [int(v) for v in out["y"]] == loops_reference(x)
+    other = LOOPS.replace("loops(", "loops2(").replace("int* y", "int* z").replace("y[t]", "z[t]")
+    src, _ = hf.fuse(LOOPS, other, 64, 64, style="structured")
+    assert hf.check(src).startswith("ok")
+    assert len(hf.Module.fused(LOOPS, other, 64, 64).cubin) > 1000
