@@ -342,6 +342,7 @@ def main():
     results = []
     fused = {}
     pgrid = {}
+    two_grids = {}
     t_setup = time.perf_counter()
     for a, b in pair_list:
         r, grid, trace = None, None, []
@@ -366,6 +367,22 @@ def main():
                       stream=stream)
         two = hf.time("two_stream", unfused[a], unfused[b], img, ga, gb, warmup=5, reps=60, flush_l2=flush,
                       stream=stream)
+        # the two-stream baseline gets the same grid freedom as the fused kernel: every
+        # (grid_a, grid_b) combination is screened and the best one re-timed like the others
+        # (concurrent kernels share the SMs, so the members' best grids alone need not be the
+        # pair's best; profiles/r01_probe_two_stream_grids.json)
+        screen = {(x, y): hf.time("two_stream", unfused[a], unfused[b], img, x, y, warmup=2, reps=15,
+                                  flush_l2=flush, stream=stream)["iqm_us"]
+                  for x in grids for y in grids if (x, y) != (ga, gb)}
+        tga, tgb = ga, gb
+        if screen:
+            bx, by = min(screen, key=screen.get)
+            if screen[(bx, by)] < two["iqm_us"]:
+                alt = hf.time("two_stream", unfused[a], unfused[b], img, bx, by, warmup=5, reps=60,
+                              flush_l2=flush, stream=stream)
+                if alt["iqm_us"] < two["iqm_us"]:
+                    two, tga, tgb = alt, bx, by
+        two_grids[(a, b)] = (tga, tgb)
         ta = hf.time("single", unfused[a], None, img, ga, warmup=2, reps=10, flush_l2=flush, stream=stream)
         tb = hf.time("single", unfused[b], None, img, gb, warmup=2, reps=10, flush_l2=flush, stream=stream)
         # baselines of the paper's comparison: the reference's naive goto fusion of the naive
@@ -378,7 +395,7 @@ def main():
                  for g in grids)
         results.append({"pair": f"{a}+{b}", "grid": grid, "d0": r["d1"] + r["d2"], "d1": r["d1"], "d2": r["d2"],
                         "reg_cap": cap,
-                        "grid_a": ga, "grid_b": gb,
+                        "grid_a": ga, "grid_b": gb, "two_stream_grids": [tga, tgb],
                         "bytes": work[a].bytes + work[b].bytes, "regs": m.info.regs,
                         "blocks_per_sm": m.info.blocks_per_sm, "fused_us": fz["iqm_us"],
                         "seq_us": seq["iqm_us"], "two_stream_us": two["iqm_us"],
@@ -424,11 +441,13 @@ def main():
     side = torch.cuda.Stream()
 
     def unfused_step():
-        # the same ten pairs unfused, each pair's two kernels concurrent on two streams
+        # the same ten pairs unfused, each pair's two kernels concurrent on two streams (at the
+        # pair's best two-stream grids)
         for a, b in pair_list:
+            ga, gb = two_grids[(a, b)]
             side.wait_stream(stream)
-            unfused[a].run(img, mgrid[a], stream)
-            unfused[b].run(img, mgrid[b], side)
+            unfused[a].run(img, ga, stream)
+            unfused[b].run(img, gb, side)
             stream.wait_stream(side)
         if dist is not None:
             reduce_outputs()
@@ -657,10 +676,18 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
                                 specialize=img)
         t = {mode: hf.time(mode, ka, kb, img, ga, gb, warmup=2, reps=10, stream=stream)["iqm_us"]
              for mode in ("sequential", "two_stream")}
+        two_g = (ga, gb)
+        for x in cgrids:  # the two-stream baseline at its best grid pair (as for the DL pairs)
+            for y in cgrids:
+                if (x, y) != (ga, gb):
+                    tt = hf.time("two_stream", ka, kb, img, x, y, warmup=2, reps=10, stream=stream)["iqm_us"]
+                    if tt < t["two_stream"]:
+                        t["two_stream"], two_g = tt, (x, y)
         tf = hf.time("single", m, None, img, grid_f, warmup=2, reps=10, stream=stream)["iqm_us"]
         ta = hf.time("single", ka, None, img, ga, warmup=2, reps=10, stream=stream)["iqm_us"]
         tb = hf.time("single", kb, None, img, gb, warmup=2, reps=10, stream=stream)["iqm_us"]
-        res = {"pair": f"{a}+{b}", "grid": grid_f, "grid_a": ga, "grid_b": gb, "d1": r["d1"], "d2": r["d2"],
+        res = {"pair": f"{a}+{b}", "grid": grid_f, "grid_a": ga, "grid_b": gb, "two_stream_grids": list(two_g),
+               "d1": r["d1"], "d2": r["d2"],
                "reg_cap": r["reg_cap"],
                "interval_regs": r["interval_regs"], "regs": m.info.regs,
                "blocks_per_sm": m.info.blocks_per_sm, "a_us": ta, "b_us": tb, "seq_us": t["sequential"],
@@ -689,27 +716,43 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
         res["winning_nonce"] = win.tolist()
         out["c3"].append(res)
         del img, img_out
-    # C4: Upsample + Blake256
+    # C4: Upsample + Blake256. Every variant at its best launch grid from the DL grid set:
+    # each member alone (sequential), every grid pair (two-stream), every grid for the fused
+    # kernel's search
+    c4_grids = [296, 592, 1184, 2368]
     wu = P.MEMBERS["upsample"].sizes["full"](rank)
-    wb = CR.workload("blake256", 1 << 21, grid, nonce0=0, target=1 << 12)
+    wb = CR.workload("blake256", 1 << 21, max(c4_grids), nonce0=0, target=1 << 12)
     img = hf.Image(wu.image).merge(hf.Image(wb.image)).upload(stream)
     su = P.source("b200", "upsample")
     ku = hf.Module.kernel(su, grid=grid, specialize=img)
     kb = hf.Module.kernel(srcs["blake256"], grid=grid, specialize=img)
-    seq = hf.time("sequential", ku, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
-    two = hf.time("two_stream", ku, kb, img, grid, grid, warmup=2, reps=10, stream=stream)["iqm_us"]
+    alone = {}
+    for name, k in (("upsample", ku), ("blake256", kb)):
+        ts = {g: hf.time("single", k, None, img, g, warmup=2, reps=10, stream=stream)["iqm_us"] for g in c4_grids}
+        alone[name] = min(ts, key=ts.get)
+    gu, gbk = alone["upsample"], alone["blake256"]
+    seq = hf.time("sequential", ku, kb, img, gu, gbk, warmup=2, reps=10, stream=stream)["iqm_us"]
+    two, two_g = None, None
+    for x in c4_grids:
+        for y in c4_grids:
+            tt = hf.time("two_stream", ku, kb, img, x, y, warmup=2, reps=10, stream=stream)["iqm_us"]
+            if two is None or tt < two:
+                two, two_g = tt, [x, y]
     sweep = []
-    for d0 in (640, 768, 896, 1024):
-        try:
-            r = hf.search(su, srcs["blake256"], img, d0=d0, grid=grid, reps=5, warmup=2, specialize=True,
-                          extra_caps=(32, 40, 48, 64, 96), interval_regs=True)
-        except hf.HFuseError:
-            continue
-        for row in r["trace"]:
-            sweep.append({"d0": d0, "d1": row["d1"], "reg_cap": row["reg_cap"], "us": round(row["us"], 2),
-                          "occupancy": round(row["occupancy"], 3)})
+    for g in c4_grids:
+        for d0 in (640, 768, 896, 1024):
+            try:
+                r = hf.search(su, srcs["blake256"], img, d0=d0, grid=g, reps=5, warmup=2, specialize=True,
+                              extra_caps=(32, 40, 48, 64, 96), interval_regs=True)
+            except hf.HFuseError:
+                continue
+            for row in r["trace"]:
+                sweep.append({"grid": g, "d0": d0, "d1": row["d1"], "reg_cap": row["reg_cap"],
+                              "interval_regs": row.get("interval_regs"), "us": round(row["us"], 2),
+                              "occupancy": round(row["occupancy"], 3)})
     best = min(sweep, key=lambda x: x["us"])
-    out["c4"] = {"pair": "upsample+blake256", "seq_us": seq, "two_stream_us": two, "best": best,
+    out["c4"] = {"pair": "upsample+blake256", "seq_us": seq, "two_stream_us": two, "grid_a": gu, "grid_b": gbk,
+                 "two_stream_grids": two_g, "best": best,
                  "speedup": min(seq, two) / best["us"], "sweep": sweep}
     # C4 pair roofline: max(Upsample's HBM time, BLAKE-256's issue time)
     rb = crypto_roofline({"blake256": 1 << 21}, best["us"], sm_mhz, hbm_peak)

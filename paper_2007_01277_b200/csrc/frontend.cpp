@@ -580,7 +580,7 @@ class Parser {
             }
             return for_loop(p, n);
           }
-          if ((at_ident("vload") || at_ident("vstore")) && at(T::LParen, 1))
+          if ((at_ident("vload") || at_ident("vstore") || at_ident("vstore_cs")) && at(T::LParen, 1))
             return vector_access(p);
           if (at_ident("atomic_add_release") && at(T::LParen, 1)) {
             // release-ordered atomic add: earlier writes of this thread are visible to whoever
@@ -626,12 +626,16 @@ class Parser {
     }
   }
 
-  // vload(arr, i, d0, .., dn-1) / vstore(arr, i, e0, .., en-1), n in {2, 4}
+  // vload(arr, i, d0, .., dn-1) / vstore(arr, i, e0, .., en-1), n in {2, 4};
+  // vstore_cs: the same store marked streaming (L2 evict-first on sm_100a: an output no later
+  // access of the kernel reads); the interpreter and the lowering treat it as vstore
   Stmt vector_access(Pos p) {
     Stmt s;
     s.pos = p;
-    bool load = next().text == "vload";
+    const std::string op = next().text;
+    bool load = op == "vload";
     s.k = load ? SK::VLoad : SK::VStore;
+    s.bid = op == "vstore_cs" ? 1 : 0;
     want(T::LParen);
     Tok arr = want(T::Ident);
     s.name = arr.text;

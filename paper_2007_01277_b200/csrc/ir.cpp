@@ -242,6 +242,7 @@ bool same_stmt(const Stmt& a, const Stmt& b) {
   if (a.k != b.k || a.name != b.name || a.outs != b.outs || a.has_alt != b.has_alt) return false;
   if (a.k == SK::Decl && a.ty != b.ty) return false;
   if (a.k == SK::BarSync && (a.bid != b.bid || a.bcount != b.bcount)) return false;
+  if ((a.k == SK::Atomic || a.k == SK::VStore) && a.bid != b.bid) return false;
   if (a.k == SK::For && a.unroll != b.unroll) return false;
   return same_exprs(a.idx, b.idx) && same_exprs(a.val, b.val) && same(a.body, b.body) &&
          same(a.alt, b.alt) && same(a.init, b.init) && same(a.step, b.step);
@@ -546,7 +547,7 @@ struct MkPrinter {
         break;
       case SK::VStore:
         pad(ind);
-        o += "vstore(" + s.name + ", ";
+        o += std::string(s.bid == 1 ? "vstore_cs(" : "vstore(") + s.name + ", ";
         expr(s.idx[0]);
         for (const auto& v : s.val) {
           o += ", ";

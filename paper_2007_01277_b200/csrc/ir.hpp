@@ -110,7 +110,7 @@ struct Stmt {
   std::vector<Stmt> body, alt;    // If then/else; loop body
   std::vector<Stmt> init, step;   // For header (one statement each)
   bool has_alt = false;
-  int bid = 0, bcount = 0;        // BarSync; Atomic: bid 1 = atomic_add_release (MK+)
+  int bid = 0, bcount = 0;        // BarSync; Atomic: bid 1 = atomic_add_release (MK+); VStore: bid 1 = vstore_cs
   int unroll = 0;                 // For (MK+): 0 = no hint, -1 = `unroll`, N = `unroll N`
 };
 using Block = std::vector<Stmt>;

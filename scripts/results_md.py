@@ -32,10 +32,12 @@ if d.get("crypto"):
             "cap %s" % p["reg_cap"] if p["reg_cap"] else "uncapped (%d)" % p["regs"])
         r = p.get("roofline") or {}
         o.append(f"| {p['pair']} | {p['d1']}/{p['d2']} | {regs} | {p['fused_us']:.0f} | {p['seq_us']:.0f} | "
-                 f"{p['two_stream_us']:.0f} | **{p['speedup']:.3f}** | {r.get('frac', 0):.2f} issue, {r.get('alu_frac', 0):.2f} ALU pipe |")
+                 f"{p['two_stream_us']:.0f} | {'**%.3f**' % p['speedup'] if p['speedup'] > 1.0 else '%.3f' % p['speedup']} | {r.get('frac', 0):.2f} issue, {r.get('alu_frac', 0):.2f} ALU pipe |")
     c4 = d["crypto"]["c4"]
     b = c4["best"]
     o.append("")
+    grids = (f" (grids: fused {b['grid']}, members alone {c4['grid_a']}/{c4['grid_b']}, two-stream "
+             f"{c4['two_stream_grids'][0]}/{c4['two_stream_grids'][1]})" if "grid" in b else "")
     o.append(f"C4 Upsample + BLAKE-256: best d0 {b['d0']} (Upsample {b['d1']}), reg_cap {b['reg_cap']}: {b['us']:.1f} µs vs "
-             f"{c4['seq_us']:.1f} sequential / {c4['two_stream_us']:.1f} two-stream — **{c4['speedup']:.3f}×**.")
+             f"{c4['seq_us']:.1f} sequential / {c4['two_stream_us']:.1f} two-stream{grids} — **{c4['speedup']:.3f}×**.")
 print("\n".join(o))

@@ -222,3 +222,16 @@ def test_addc_is_the_high_word_of_a_64_bit_add(hf, tmp_path):
     assert np.array_equal(np.asarray(out["oh"], np.int64) & 0xFFFFFFFF, (s >> 32) & 0xFFFFFFFF)
     assert np.array_equal(np.asarray(out["ol"], np.int64) & 0xFFFFFFFF, s & 0xFFFFFFFF)
     assert "add.cc.u32" in hf.emit_kernel(ADDC)
+
+
+def test_vstore_cs_is_a_streaming_vstore(hf):
+    """vstore_cs: same semantics as vstore (the lowering is identical), printed back as written,
+    kept through fusion, emitted as an evict-first __stcs store on sm_100a."""
+    cs = MKPLUS.replace("vstore(fo", "vstore_cs(fo")
+    assert hf.lower(cs) == hf.lower(MKPLUS)
+    assert "vstore_cs(fo, t" in hf.normalize(cs)
+    assert "__stcs(reinterpret_cast<float4*>(fo)" in hf.emit_kernel(cs)
+    assert "__stcs" not in hf.emit_kernel(MKPLUS)
+    other = MKPLUS.replace("kernel ext(", "kernel ext2(")
+    fused, _ = hf.fuse(cs, other, 32, 32, style="structured")
+    assert fused.count("vstore_cs(") == 1 and fused.count("vstore(") == 1
