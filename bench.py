@@ -22,6 +22,7 @@ stats all-gather), timed inside the step.
 """
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -279,6 +280,8 @@ def main():
                     help="split step of the partition sweep (the reference sweeps 128)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pairs", default="all")
+    ap.add_argument("--ratios", default="0.5,1,2",
+                    help="workload-ratio study: t_b/t_a targets for every DL pair ('none' to skip)")
     ap.add_argument("--no-crypto", action="store_true", help="skip the C3/C4 crypto suite")
     ap.add_argument("--l2", default="steady", choices=["steady", "flush"],
                     help="DL timing protocol: steady = repetitions back to back with every pair's inputs "
@@ -365,23 +368,7 @@ def main():
         fz = hf.time("single", m, None, img, grid, warmup=5, reps=60, flush_l2=flush, stream=stream)
         seq = hf.time("sequential", unfused[a], unfused[b], img, ga, gb, warmup=5, reps=60, flush_l2=flush,
                       stream=stream)
-        two = hf.time("two_stream", unfused[a], unfused[b], img, ga, gb, warmup=5, reps=60, flush_l2=flush,
-                      stream=stream)
-        # the two-stream baseline gets the same grid freedom as the fused kernel: every
-        # (grid_a, grid_b) combination is screened and the best one re-timed like the others
-        # (concurrent kernels share the SMs, so the members' best grids alone need not be the
-        # pair's best; profiles/r01_probe_two_stream_grids.json)
-        screen = {(x, y): hf.time("two_stream", unfused[a], unfused[b], img, x, y, warmup=2, reps=15,
-                                  flush_l2=flush, stream=stream)["iqm_us"]
-                  for x in grids for y in grids if (x, y) != (ga, gb)}
-        tga, tgb = ga, gb
-        if screen:
-            bx, by = min(screen, key=screen.get)
-            if screen[(bx, by)] < two["iqm_us"]:
-                alt = hf.time("two_stream", unfused[a], unfused[b], img, bx, by, warmup=5, reps=60,
-                              flush_l2=flush, stream=stream)
-                if alt["iqm_us"] < two["iqm_us"]:
-                    two, tga, tgb = alt, bx, by
+        two, tga, tgb = best_two_stream(hf, unfused[a], unfused[b], img, ga, gb, grids, flush, stream)
         two_grids[(a, b)] = (tga, tgb)
         ta = hf.time("single", unfused[a], None, img, ga, warmup=2, reps=10, flush_l2=flush, stream=stream)
         tb = hf.time("single", unfused[b], None, img, gb, warmup=2, reps=10, flush_l2=flush, stream=stream)
@@ -519,6 +506,10 @@ def main():
         e2e["h2d_bytes_per_step"] *= world
         e2e["d2h_bytes_per_step"] *= world
     del img  # free the DL images before the crypto suite (the Ethash DAG alone is 4 GiB)
+    ratio_res = None
+    if world == 1 and args.ratios != "none":  # a one-GPU study (C2); shards run only the step
+        member_us = {k: min(v.values()) for k, v in member_sweep.items()}
+        ratio_res = ratio_study(hf, P, pair_list, src, shape, rank, grids, d0s, flush, stream, member_us, args)
     crypto_res = None
     clk = clocks.summary()
     if not args.no_crypto:
@@ -590,6 +581,7 @@ def main():
         "cpu_baseline": cpu,
         "setup_s": round(setup_s, 1),
         "search": {r["pair"]: r["search_trace"] for r in results},
+        "ratios": ratio_res,
         "crypto": crypto_res,
     }
     print(json.dumps(line), flush=True)
@@ -763,6 +755,87 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
                                  "frac": t_roof / best["us"], "hbm_us": t_hbm, "issue_us": rb["issue_us"],
                                  "alu_pipe_us": rb["alu_pipe_us"]}
     return out
+
+
+
+def best_two_stream(hf, ka, kb, img, ga, gb, grids, flush, stream):
+    """The two-stream baseline with the same grid freedom as the fused kernel: timed at the
+    members' best grids alone, every other (grid_a, grid_b) pair screened with 15 repetitions
+    and the best re-timed like the rest (concurrent kernels share the SMs, so the members' best
+    grids alone need not be the pair's best; profiles/r01_probe_two_stream_grids.json).
+    Returns (timing dict, grid_a, grid_b)."""
+    two = hf.time("two_stream", ka, kb, img, ga, gb, warmup=5, reps=60, flush_l2=flush, stream=stream)
+    screen = {(x, y): hf.time("two_stream", ka, kb, img, x, y, warmup=2, reps=15, flush_l2=flush,
+                              stream=stream)["iqm_us"]
+              for x in grids for y in grids if (x, y) != (ga, gb)}
+    if screen:
+        bx, by = min(screen, key=screen.get)
+        if screen[(bx, by)] < two["iqm_us"]:
+            alt = hf.time("two_stream", ka, kb, img, bx, by, warmup=5, reps=60, flush_l2=flush, stream=stream)
+            if alt["iqm_us"] < two["iqm_us"]:
+                return alt, bx, by
+    return two, ga, gb
+
+
+def ratio_study(hf, P, pair_list, src, shape, rank, grids, d0s, flush, stream, member_us, args):
+    """The paper's workload-ratio experiment: every pair with
+    its second member's batch rescaled so the unfused times stand at t_b / t_a = r for each r in
+    --ratios, each point fused, searched exhaustively and compared like the main table (the
+    model pre-filter, K = 3, missed BN + Upsample at r = 2 by 13 %). Outside the timed step."""
+    ratios = [float(x) for x in args.ratios.split(",")]
+    rows = []
+    for a, b in pair_list:
+        for r in ratios:
+            wa = P.MEMBERS[a].sizes[shape](rank)
+            f = r * member_us[a] / member_us[b]
+            for attempt in range(2):
+                # batch scale from the natural-size times, then one correction from the
+                # measured ratio (a launch's fixed cost makes time not quite linear in batch)
+                wb, nb = P.scaled(b, f, shape, seed=rank)
+                img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload(stream)
+                ka = hf.Module.kernel(src[a], grid=grids[0], specialize=img)
+                kb = hf.Module.kernel(src[b], grid=grids[0], specialize=img)
+                alone = {}
+                for name, k in ((a, ka), (b, kb)):
+                    ts = {g: hf.time("single", k, None, img, g, warmup=2, reps=10, flush_l2=flush,
+                                     stream=stream)["iqm_us"] for g in grids}
+                    g = min(ts, key=ts.get)
+                    alone[name] = (g, ts[g])
+                got = alone[b][1] / alone[a][1]
+                if attempt == 1 or abs(got / r - 1.0) <= 0.05:
+                    break
+                f_next = f * r / got
+                if P.scaled(b, f_next, shape)[1] == nb:
+                    break
+                f = f_next
+                del ka, kb, img
+            best, grid = None, None
+            for d0 in d0s:
+                for g in grids if d0 == 1024 else [2 * x for x in grids]:
+                    rg = hf.search(src[a], src[b], img, d0=d0, grid=g, reps=args.search_reps, warmup=2,
+                                   specialize=True, flush_l2=flush, granularity=args.granularity)
+                    if best is None or rg["best_time"] < best["best_time"]:
+                        best, grid = rg, g
+            cap = best["reg_cap"]
+            m = hf.Module.fused(src[a], src[b], best["d1"], best["d2"], regcap=cap if cap else "off", grid=grid,
+                                specialize=img)
+            tf = hf.time("single", m, None, img, grid, warmup=5, reps=60, flush_l2=flush, stream=stream)["iqm_us"]
+            (ga, ta), (gb, tb) = alone[a], alone[b]
+            seq = hf.time("sequential", ka, kb, img, ga, gb, warmup=5, reps=60, flush_l2=flush, stream=stream)["iqm_us"]
+            two, tga, tgb = best_two_stream(hf, ka, kb, img, ga, gb, grids, flush, stream)
+            rows.append({"pair": f"{a}+{b}", "target_ratio": r, "ratio": round(tb / ta, 3), "batch_b": nb,
+                         "a_us": round(ta, 2), "b_us": round(tb, 2), "grid": grid, "d0": best["d1"] + best["d2"],
+                         "d1": best["d1"], "d2": best["d2"], "reg_cap": cap, "fused_us": round(tf, 2),
+                         "seq_us": round(seq, 2), "two_stream_us": round(two["iqm_us"], 2),
+                         "two_stream_grids": [tga, tgb], "speedup": round(min(seq, two["iqm_us"]) / tf, 4)})
+            del m, ka, kb, img
+    geo = {}
+    for r in ratios:
+        sp = [x["speedup"] for x in rows if x["target_ratio"] == r]
+        geo[str(r)] = math.exp(sum(math.log(v) for v in sp) / len(sp)) if sp else None
+    return {"how": "second member's batch scaled to t_b/t_a = r (members timed alone at their best grids); "
+                   "fused search over d0 x grids x splits x caps (exhaustive); "
+                   "two-stream at its best grid pair", "rows": rows, "speedup_geomean": geo}
 
 
 def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):

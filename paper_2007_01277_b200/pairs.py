@@ -133,3 +133,30 @@ MEMBERS: Dict[str, Member] = {
 ORDER = ["bn", "hist", "im2col", "maxpool", "upsample"]
 # The ten DL pairs of the paper.
 PAIRS = [(a, b) for i, a in enumerate(ORDER) for b in ORDER[i + 1:]]
+
+# Batch-scaled members for the paper's workload-ratio study (each pair is
+# reported at several execution-time ratios of its two kernels): the batch dimension of a
+# member's C2 / conv3_x shape, as (workload of batch n, default batch n).
+BATCHED: Dict[str, Dict[str, tuple]] = {
+    "full": {
+        "bn": (lambda n: _bn(n, 256, 56 * 56), 64),
+        "hist": (lambda n: _hist(n * 256 * 56 * 56), 64),
+        "im2col": (lambda n: _im2col(n * 64, 56, 56), 32),
+        "maxpool": (lambda n: _maxpool(n * 64, 112, 112), 64),
+        "upsample": (lambda n: _upsample(n * 256, 28, 28), 64),
+    },
+    "conv3": {
+        "bn": (lambda n: _bn(n, 512, 28 * 28), 64),
+        "hist": (lambda n: _hist(n * 512 * 28 * 28), 64),
+        "im2col": (lambda n: _im2col(n * 128, 28, 28), 32),
+        "maxpool": (lambda n: _maxpool(n * 128, 56, 56), 64),
+        "upsample": (lambda n: _upsample(n * 512, 14, 14), 64),
+    },
+}
+
+
+def scaled(key: str, factor: float, shape: str = "full", seed: int = 0) -> "tuple[Workload, int]":
+    """Member `key` at `factor` times its default batch (rounded, at least 1): (workload, batch)."""
+    make, n0 = BATCHED[shape][key]
+    n = max(1, int(round(n0 * factor)))
+    return make(n)(seed), n

@@ -23,6 +23,24 @@ o.append(f"Geomean speedup vs min(seq, two-stream): {d['speedup_geomean']:.3f}. 
          + (f"reference CPU interpreter: {d['cpu_baseline']['value'] / 1e6:.1f} s per step "
             f"({d['cpu_baseline']['cores']} processes). " if d.get("cpu_baseline") else "") +
          f"Clocks {d['clocks']['sm_mhz']:.0f}/{d['clocks']['sm_max_mhz']:.0f} MHz, reasons {d['clocks']['reasons']}.")
+if d.get("ratios"):
+    rr = d["ratios"]
+    rs = sorted({x["target_ratio"] for x in rr["rows"]})
+    o.append("")
+    o.append("Cells: measured t_b/t_a; fused µs / min(seq, two-stream) µs; speedup.")
+    o.append("")
+    o.append("| pair | " + " | ".join(f"t_b/t_a ≈ {r:g}" for r in rs) + " |")
+    o.append("|---|" + "---|" * len(rs))
+    for pair in dict.fromkeys(x["pair"] for x in rr["rows"]):
+        cells = []
+        for r in rs:
+            x = next(x for x in rr["rows"] if x["pair"] == pair and x["target_ratio"] == r)
+            sp = x["speedup"]
+            cells.append(f"{x['ratio']:.2f}, {x['fused_us']:.1f} / {min(x['seq_us'], x['two_stream_us']):.1f}, "
+                         + ("**%.3f**" % sp if sp > 1.0 else "%.3f" % sp))
+        o.append(f"| {pair} | " + " | ".join(cells) + " |")
+    o.append("")
+    o.append("Geomean speedup per ratio: " + ", ".join(f"{k}: {v:.3f}" for k, v in rr["speedup_geomean"].items()) + ".")
 if d.get("crypto"):
     o.append("")
     o.append("| crypto pair | partition | registers | fused µs | seq µs | 2-stream µs | speedup | roofline (bound) |")
