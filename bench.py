@@ -389,6 +389,7 @@ def main():
                         "a_us": ta["iqm_us"], "b_us": tb["iqm_us"],
                         "naive_fused_us": tn["iqm_us"], "vertical_us": tv,
                         "search_trace": trace})
+    stream_ceilings(hf, P, results, work, grids, flush, stream)
     setup_s = time.perf_counter() - t_setup
 
     import ctypes
@@ -756,6 +757,33 @@ def crypto_suite(hf, torch, args, rank, world, stream, sm_mhz=None, hbm_peak=655
                                  "alu_pipe_us": rb["alu_pipe_us"]}
     return out
 
+
+
+def stream_ceilings(hf, P, results, work, grids, flush, stream):
+    """Mix-matched HBM ceiling of every pair: plain 128-bit streaming kernels
+    (kernels/probe/stream*.mk, one or four loads in flight per thread) reading and writing the
+    pair's algorithmic read / write bytes, best over both forms and the fused grids, timed under
+    the same protocol as the pairs. Adds ceiling_us / ceiling_frac (= ceiling / fused) to each
+    result: how close the fused kernel is to what HBM delivers for that read:write mix and
+    size, where the copy roofline assumes one fixed mix."""
+    forms = {k: open(os.path.join(P.KERNELS, "probe", k + ".mk")).read() for k in ("stream", "stream4")}
+    for res in results:
+        a, b = res["pair"].split("+")
+        r, w = work[a].read + work[b].read, work[a].write + work[b].write
+        img = hf.Image(f"array s_src float32 {r // 4} zero\narray s_dst float32 {max(w, 64) // 4} zero\n"
+                       f"scalar s_nr4 int32 {r // 16}\nscalar s_nw4 int32 {w // 16}\n").upload(stream)
+        best = None
+        for name, text in forms.items():
+            m = hf.Module.kernel(text, grid=grids[0], specialize=img)
+            for g in sorted(set(grids) | {2 * x for x in grids}):
+                t = hf.time("single", m, None, img, g, warmup=3, reps=30, flush_l2=flush, stream=stream)["iqm_us"]
+                if best is None or t < best[0]:
+                    best = (t, name, g)
+            del m
+        res["ceiling_us"] = best[0]
+        res["ceiling_kernel"] = f"{best[1]}@{best[2]}"
+        res["ceiling_frac"] = best[0] / res["fused_us"]
+        del img
 
 
 def best_two_stream(hf, ka, kb, img, ga, gb, grids, flush, stream):

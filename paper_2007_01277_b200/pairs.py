@@ -25,6 +25,11 @@ class Workload:
     image: str        # memory-image text
     bytes: int        # algorithmic bytes per launch (reads + writes)
     desc: str
+    write: int = 0    # of which written
+
+    @property
+    def read(self) -> int:
+        return self.bytes - self.write
 
 
 @dataclass
@@ -50,7 +55,7 @@ def _bn(N: int, C: int, HW: int, slots: int = BN_SLOTS) -> Callable[[int], Workl
                f"array bn_pm float32 {slots * C} zero\narray bn_cnt int32 {C} zero\n"
                f"scalar bn_N int32 {N}\nscalar bn_C int32 {C}\nscalar bn_HW int32 {HW}\n"
                f"scalar bn_P int32 {slots}\n")
-        return Workload(img, 4 * n + 8 * C, f"bn_stats x[{N},{C},{HW}] fp32")
+        return Workload(img, 4 * n + 8 * C, f"bn_stats x[{N},{C},{HW}] fp32", 8 * C)
     return make
 
 
@@ -58,7 +63,7 @@ def _hist(n: int, lo: float = -4.0, hi: float = 4.0) -> Callable[[int], Workload
     def make(seed: int = 0) -> Workload:
         img = (f"array hi_x float32 {n} seed {2 + seed} uniform {lo:g} {hi:g}\n"
                f"array hi_out int32 64 zero\nscalar hi_n int32 {n}\n")
-        return Workload(img, 4 * n + 4 * 64, f"hist 64 bins over [-4,4], {n} fp32")
+        return Workload(img, 4 * n + 4 * 64, f"hist 64 bins over [-4,4], {n} fp32", 4 * 64)
     return make
 
 
@@ -70,7 +75,7 @@ def _maxpool(NC: int, H: int, W: int) -> Callable[[int], Workload]:
                f"array mp_y float32 {m} zero\narray mp_idx int32 {m} zero\n"
                f"scalar mp_NC int32 {NC}\nscalar mp_H int32 {H}\nscalar mp_W int32 {W}\n"
                f"scalar mp_OH int32 {OH}\nscalar mp_OW int32 {OW}\n")
-        return Workload(img, 4 * n + 8 * m, f"maxpool 3x3/s2/p1 x[{NC},{H},{W}] fp32 + int32 idx")
+        return Workload(img, 4 * n + 8 * m, f"maxpool 3x3/s2/p1 x[{NC},{H},{W}] fp32 + int32 idx", 8 * m)
     return make
 
 
@@ -82,7 +87,7 @@ def _upsample(NC: int, IH: int, IW: int) -> Callable[[int], Workload]:
                f"array us_y float32 {m} zero\n"
                f"scalar us_NC int32 {NC}\nscalar us_IH int32 {IH}\nscalar us_IW int32 {IW}\n"
                f"scalar us_OH int32 {OH}\nscalar us_OW int32 {OW}\n")
-        return Workload(img, 4 * n + 4 * m, f"upsample bilinear 2x x[{NC},{IH},{IW}] fp32")
+        return Workload(img, 4 * n + 4 * m, f"upsample bilinear 2x x[{NC},{IH},{IW}] fp32", 4 * m)
     return make
 
 
@@ -92,7 +97,7 @@ def _im2col(NC: int, H: int, W: int) -> Callable[[int], Workload]:
         img = (f"array ic_x float32 {n} seed {5 + seed} uniform -1 1\n"
                f"array ic_col float32 {m} zero\n"
                f"scalar ic_NC int32 {NC}\nscalar ic_H int32 {H}\nscalar ic_W int32 {W}\n")
-        return Workload(img, 4 * n + 4 * m, f"im2col 3x3/p1 x[{NC},{H},{W}] fp32")
+        return Workload(img, 4 * n + 4 * m, f"im2col 3x3/p1 x[{NC},{H},{W}] fp32", 4 * m)
     return make
 
 

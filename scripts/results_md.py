@@ -4,13 +4,17 @@ import sys
 
 d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
 o = []
-o.append("| pair | grid | d1/d2 | fused µs | seq µs | 2-stream µs | speedup | roofline | naive goto fusion µs | VFuse µs |")
-o.append("|---|---|---|---|---|---|---|---|---|---|")
+ceil = all("ceiling_frac" in p for p in d["pairs"])
+o.append("| pair | grid | d1/d2 | fused µs | seq µs | 2-stream µs | speedup | roofline |" + (" mix ceiling µs (frac) |" if ceil else "")
+         + " naive goto fusion µs | VFuse µs |")
+o.append("|---|---|---|---|---|---|---|---|---|---|" + ("---|" if ceil else ""))
 for p in d["pairs"]:
     sp = p["speedup"]
     o.append(f"| {p['pair']} | {p['grid']} | {p['d1']}/{p['d2']}{' cap ' + str(p['reg_cap']) if p['reg_cap'] else ''} | "
              f"{p['fused_us']:.1f} | {p['seq_us']:.1f} | {p['two_stream_us']:.1f} | "
-             f"{'**%.3f**' % sp if sp > 1.0 else '%.3f' % sp} | {p['roofline_frac']:.3f} | {p['naive_fused_us']:.1f} | {p['vertical_us']:.1f} |")
+             f"{'**%.3f**' % sp if sp > 1.0 else '%.3f' % sp} | {p['roofline_frac']:.3f} | "
+             + (f"{p['ceiling_us']:.1f} ({p['ceiling_frac']:.3f}) | " if ceil else "")
+             + f"{p['naive_fused_us']:.1f} | {p['vertical_us']:.1f} |")
 o.append("")
 o.append(f"Geomean speedup vs min(seq, two-stream): {d['speedup_geomean']:.3f}. Step of all ten (`value`): "
          f"{d['value']:.1f} µs fused (programmatic dependent launches) vs "
