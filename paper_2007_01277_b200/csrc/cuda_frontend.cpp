@@ -16,7 +16,8 @@
 //   stmts     declarations (several declarators, initializers), `__shared__ T s[N]` (N a constant
 //             expression), `=` and compound assignments, `++`/`--`, if/else, for, while, return,
 //             vector loads/stores `reinterpret_cast<const float4*>(p)[i]` / `((float4*)p)[i]`
-//             (MK+ vload/vstore), `make_float4(..)`, `__ldg(&a[i])`,
+//             (MK+ vload/vstore), `__stcs(reinterpret_cast<float4*>(p) + i, v)` (vstore_cs),
+//             `make_float4(..)`, `__ldg(&a[i])`,
 //             `{ }` blocks, break / continue (gotos to per-loop labels), `__syncthreads()`,
 //             `__syncwarp()`, `__threadfence()`,
 //             `atomicAdd(&a[i], v)` as a statement, device-function calls, `#pragma unroll [N]`
@@ -590,6 +591,22 @@ class Translator {
       put("atomic_add(" + lv + ", " + conv(v, lt, p).t + ");", p);
       return;
     }
+    if (is_id("__stcs") && is_op("(", 1)) {  // __stcs(vecptr + i, v): streaming vector store
+      Pos sp = peek().pos;
+      next();
+      want_op("(");
+      VRef r = vector_base();
+      want_op("+");
+      CE i = expr();
+      want_op(",");
+      std::vector<std::string> vals = vector_value(r.ty, sp);
+      want_op(")");
+      want_op(";");
+      std::string o = "vstore_cs(" + r.arr + ", " + conv(i, 'i', sp).t;
+      for (const auto& v : vals) o += ", " + v;
+      put(o + ");", p);
+      return;
+    }
     if (at_vector_ref()) {  // vector store
       Pos sp = peek().pos;
       auto [arr, idx, vt] = vector_ref();
@@ -670,6 +687,17 @@ class Translator {
   };
   VRef vector_ref() {
     Pos p = peek().pos;
+    VRef r = vector_base();
+    want_op("[");
+    CE i = expr();
+    want_op("]");
+    r.idx = conv(i, 'i', p).t;
+    return r;
+  }
+
+  // the vector-typed pointer of a vector reference: reinterpret_cast<T*>(p) or ((T*)p)
+  VRef vector_base() {
+    Pos p = peek().pos;
     CT ty;
     std::string arr;
     if (is_id("reinterpret_cast")) {
@@ -695,10 +723,7 @@ class Translator {
     auto it = arrs_.find(arr);
     if (it == arrs_.end()) fail("'" + arr + "' is not a pointer parameter or shared array", p);
     if ((it->second == 'f') != (ty.base == 'f')) fail("vector cast changes the element type of '" + arr + "'", p);
-    want_op("[");
-    CE i = expr();
-    want_op("]");
-    return VRef{arr, conv(i, 'i', p).t, ty};
+    return VRef{arr, "", ty};
   }
 
   // the components of a vector-valued expression: make_T(..), a vector variable

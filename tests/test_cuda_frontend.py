@@ -374,3 +374,16 @@ def test_cuda_break_and_continue(hf, tmp_path):
     src, _ = hf.fuse(LOOPS, other, 64, 64, style="structured")
     assert hf.check(src).startswith("ok")
     assert len(hf.Module.fused(LOOPS, other, 64, 64).cubin) > 1000
+
+
+def test_cuda_stcs_is_vstore_cs(hf):
+    src = r"""
+__global__ void __launch_bounds__(64) cp(const float* __restrict__ x, float* y) {
+  int t = threadIdx.x;
+  float4 v = reinterpret_cast<const float4*>(x)[t];
+  __stcs(reinterpret_cast<float4*>(y) + t, make_float4(v.w, v.z, v.y, v.x));
+}
+"""
+    low = hf.normalize(src)
+    assert "vstore_cs(y, t" in low
+    assert "__stcs(" in hf.emit_kernel(src)
