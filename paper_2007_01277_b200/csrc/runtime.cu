@@ -264,7 +264,9 @@ struct Prepared {
 
 Prepared prepare(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) {
   Prepared p;
-  p.opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-fmad=false"};
+  const char* contract = std::getenv("HF_FP_CONTRACT");  // probe knob, see emit_sm100.cpp
+  p.opts = {"--gpu-architecture=sm_100a", "--std=c++17",
+            contract && std::string(contract) == "1" ? "-fmad=true" : "-fmad=false"};
   if (lineinfo) p.opts.push_back("-lineinfo");
   p.source = k.source;
   if (maxrreg && k.launch_regs > 0)
