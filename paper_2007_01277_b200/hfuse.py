@@ -376,7 +376,7 @@ class Image:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:  # at interpreter exit the module globals may be gone
             _lib.hf_image_free(h)
             self._h = None
 
@@ -513,7 +513,7 @@ class Module:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:
             _lib.hf_module_free(h)
             self._h = None
 
