@@ -911,7 +911,9 @@ def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):
                 ups.append((d, h))
             downs.append((h, d))
         plan.append((m, pgrid[(a, b)], ins, ups, downs, args_))
-    s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
+    # downloads alternate over HF_E2E_DOWN_STREAMS streams (default 1; probe: more copy engines)
+    n_down = max(1, int(os.environ.get("HF_E2E_DOWN_STREAMS", "1")))
+    s_up, s_downs = torch.cuda.Stream(), [torch.cuda.Stream() for _ in range(n_down)]
     n = len(plan)
     ev_in = {name: torch.cuda.Event() for name in shared}
     ev_up = [torch.cuda.Event() for _ in range(n)]
@@ -942,6 +944,7 @@ def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):
                 stream.wait_event(ev_dn[i])       # its outputs of the previous step are downloaded
             m.launch(args_, grid=g, stream=stream)
             ev_k[i].record(stream)
+            s_down = s_downs[i % n_down]
             with torch.cuda.stream(s_down):
                 s_down.wait_event(ev_k[i])
                 for h, d in downs:
@@ -956,10 +959,12 @@ def e2e_step(hf, torch, P, pair_list, fused, work, keys, pgrid, stream, args):
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record(stream)
     s_up.wait_event(s0)
-    s_down.wait_event(s0)
+    for s_down in s_downs:
+        s_down.wait_event(s0)
     for i in range(steps):
         one_step(False)
-    stream.wait_stream(s_down)
+    for s_down in s_downs:
+        stream.wait_stream(s_down)
     s1.record(stream)
     torch.cuda.synchronize()
     us = s0.elapsed_time(s1) * 1000.0 / steps
