@@ -249,6 +249,24 @@ int hf_time(int mode, const hf_module* a, const hf_module* b, hf_image* img, int
             int grid_b, int warmup, int reps, int flush_l2, void* stream, hf_timing* out,
             hf_error* err);
 
+/* Graph-timed protocol (B200-only; replaces run_timed's per-repetition measurement for
+ * back-to-back comparisons): `reps` repetitions of the variant captured as one CUDA graph and
+ * launched `samples` times between consecutive events, no host synchronization in the timed
+ * region. Per-repetition mean / median / min / max over samples and a Student-t 95 % half-width.
+ * Nothing is flushed: every repetition's working set should exceed L2. */
+typedef struct hf_graph_timing {
+  double mean_us;
+  double median_us;
+  double min_us;
+  double max_us;
+  double ci95_us;
+  int samples;
+  int reps;
+} hf_graph_timing;
+int hf_time_graph(int mode, const hf_module* a, const hf_module* b, hf_image* img, int grid_a,
+                  int grid_b, int reps, int samples, void* stream, hf_graph_timing* out,
+                  hf_error* err);
+
 /* ProfilerBackend::evaluate (search.hpp:19-23) for one candidate on the device. */
 int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, hf_image* img,
                int grid, int warmup, int reps, int flush_l2, int specialize, hf_eval* out,

@@ -432,6 +432,18 @@ int hf_time(int mode, const hf_module* a, const hf_module* b, hf_image* img, int
   });
 }
 
+int hf_time_graph(int mode, const hf_module* a, const hf_module* b, hf_image* img, int grid_a, int grid_b,
+                  int reps, int samples, void* stream, hf_graph_timing* out, hf_error* err) {
+  return guarded(err, [&] {
+    hf::rt::Mode md = mode == HF_TIME_SEQUENTIAL ? hf::rt::Mode::Sequential
+                      : mode == HF_TIME_TWO_STREAM ? hf::rt::Mode::TwoStream
+                                                   : hf::rt::Mode::Single;
+    hf::rt::GraphTiming t =
+        hf::rt::time_graph(md, a->m, b ? &b->m : nullptr, img->img, grid_a, grid_b, reps, samples, stream);
+    *out = hf_graph_timing{t.mean_us, t.median_us, t.min_us, t.max_us, t.ci95_us, t.samples, t.reps};
+  });
+}
+
 int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, hf_image* img, int grid, int warmup,
                int reps, int flush_l2, int specialize, hf_eval* out, hf_error* err) {
   return guarded(err, [&] {

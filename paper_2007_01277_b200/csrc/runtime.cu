@@ -20,6 +20,8 @@
 #include <thread>
 #include <atomic>
 #include <numeric>
+#include <cmath>
+#include <vector>
 
 #include "runtime.hpp"
 
@@ -592,6 +594,112 @@ Timing time(Mode mode, const Module& a, const Module* b, Image& img, int grid_a,
   t.mean_us = std::accumulate(us.begin(), us.end(), 0.0) / double(us.size());
   size_t lo = sorted.size() / 4, hi = sorted.size() - sorted.size() / 4;
   t.iqm_us = std::accumulate(sorted.begin() + lo, sorted.begin() + hi, 0.0) / double(hi - lo);
+  return t;
+}
+
+namespace {
+// two-sided 95 % Student-t quantiles for 1..30 degrees of freedom
+double t95(int dof) {
+  static const double q[] = {12.706, 4.303, 3.182, 2.776, 2.571, 2.447, 2.365, 2.306, 2.262, 2.228,
+                             2.201,  2.179, 2.160, 2.145, 2.131, 2.120, 2.110, 2.101, 2.093, 2.086,
+                             2.080,  2.074, 2.069, 2.064, 2.060, 2.056, 2.052, 2.048, 2.045, 2.042};
+  if (dof < 1) return 0.0;
+  return dof <= 30 ? q[dof - 1] : 1.960;
+}
+}  // namespace
+
+GraphTiming time_graph(Mode mode, const Module& a, const Module* b, Image& img, int grid_a, int grid_b, int reps,
+                       int samples, void* stream) {
+  if (mode != Mode::Single && !b) raise(Code::InvalidArgument, "pair timing needs two modules");
+  if (reps < 1 || samples < 1) raise(Code::InvalidArgument, "graph timing needs reps >= 1 and samples >= 1");
+  if (!a.fn || (b && !b->fn)) raise(Code::Device, "module is not loaded (no GPU?)");
+  Bound ba = bind(a, img);
+  Bound bb;
+  if (b) bb = bind(*b, img);
+  int ga = grid_a > 0 ? grid_a : a.grid;
+  int gb = b ? (grid_b > 0 ? grid_b : b->grid) : 0;
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  // capture needs a stream other than the legacy default one; the caller's stream is ordered
+  // before and after the timed region through events
+  cudaStream_t cs = nullptr, s2 = nullptr;
+  HF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  if (mode == Mode::TwoStream) HF_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  cudaEvent_t fork, join, order;
+  HF_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  HF_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  HF_CUDA(cudaEventCreateWithFlags(&order, cudaEventDisableTiming));
+  std::vector<cudaEvent_t> ev(size_t(samples) + 1);
+  for (auto& e : ev) HF_CUDA(cudaEventCreate(&e));
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  auto cleanup = [&] {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    cudaEventDestroy(order);
+    if (s2) cudaStreamDestroy(s2);
+    cudaStreamDestroy(cs);
+  };
+  try {
+    HF_CUDA(cudaEventRecord(order, user));
+    HF_CUDA(cudaStreamWaitEvent(cs, order, 0));
+    HF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    for (int r = 0; r < reps; ++r) {
+      if (mode == Mode::Single) {
+        launch_raw(a, ga, ba.args.data(), cs);
+      } else if (mode == Mode::Sequential) {
+        launch_raw(a, ga, ba.args.data(), cs);
+        launch_raw(*b, gb, bb.args.data(), cs);
+      } else {
+        HF_CUDA(cudaEventRecord(fork, cs));
+        HF_CUDA(cudaStreamWaitEvent(s2, fork, 0));
+        launch_raw(a, ga, ba.args.data(), cs);
+        launch_raw(*b, gb, bb.args.data(), s2);
+        HF_CUDA(cudaEventRecord(join, s2));
+        HF_CUDA(cudaStreamWaitEvent(cs, join, 0));
+      }
+    }
+    HF_CUDA(cudaStreamEndCapture(cs, &graph));
+    HF_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    HF_CUDA(cudaGraphLaunch(exec, cs));  // warm-up: one full graph
+    HF_CUDA(cudaEventRecord(ev[0], cs));
+    for (int i = 0; i < samples; ++i) {
+      HF_CUDA(cudaGraphLaunch(exec, cs));
+      HF_CUDA(cudaEventRecord(ev[size_t(i) + 1], cs));
+    }
+    HF_CUDA(cudaEventSynchronize(ev[size_t(samples)]));
+  } catch (...) {
+    cudaStreamEndCapture(cs, &graph);  // no-op unless still capturing
+    cudaStreamSynchronize(cs);
+    cleanup();
+    throw;
+  }
+  std::vector<double> us;
+  for (int i = 0; i < samples; ++i) {
+    float ms = 0;
+    HF_CUDA(cudaEventElapsedTime(&ms, ev[size_t(i)], ev[size_t(i) + 1]));
+    us.push_back(double(ms) * 1000.0 / reps);
+  }
+  HF_CUDA(cudaEventRecord(order, cs));
+  HF_CUDA(cudaStreamWaitEvent(user, order, 0));
+  cleanup();
+  GraphTiming t;
+  t.samples = samples;
+  t.reps = reps;
+  std::vector<double> sorted = us;
+  std::sort(sorted.begin(), sorted.end());
+  t.min_us = sorted.front();
+  t.max_us = sorted.back();
+  size_t m = sorted.size();
+  t.median_us = m % 2 ? sorted[m / 2] : 0.5 * (sorted[m / 2 - 1] + sorted[m / 2]);
+  t.mean_us = std::accumulate(us.begin(), us.end(), 0.0) / double(m);
+  if (m > 1) {
+    double ss = 0;
+    for (double x : us) ss += (x - t.mean_us) * (x - t.mean_us);
+    t.ci95_us = t95(int(m) - 1) * std::sqrt(ss / double(m - 1)) / std::sqrt(double(m));
+  }
   return t;
 }
 

@@ -13,6 +13,10 @@
 #include "fuser.hpp"
 #include "image.hpp"
 
+namespace hf::rt {
+struct Module;
+}
+
 namespace hf {
 
 struct EvalOutcome {

@@ -44,7 +44,7 @@ EXPORTS = [
     "hf_module_cubin", "hf_launch", "hf_launch_ex", "hf_run_ex", "hf_module_free", "hf_image_parse", "hf_image_merge",
     "hf_image_materialize", "hf_image_upload", "hf_image_download", "hf_image_digest",
     "hf_image_serialize", "hf_image_count", "hf_image_entry", "hf_image_find",
-    "hf_image_set_host", "hf_image_bytes", "hf_image_free", "hf_run", "hf_time", "hf_profile",
+    "hf_image_set_host", "hf_image_bytes", "hf_image_free", "hf_run", "hf_time", "hf_time_graph", "hf_profile",
     "hf_search",
 ]
 
@@ -81,6 +81,11 @@ class _ModInfo(C.Structure):
 class _Timing(C.Structure):
     _fields_ = [("median_us", C.c_double), ("min_us", C.c_double), ("mean_us", C.c_double),
                 ("max_us", C.c_double), ("reps", C.c_int), ("iqm_us", C.c_double)]
+
+
+class _GraphTiming(C.Structure):
+    _fields_ = [("mean_us", C.c_double), ("median_us", C.c_double), ("min_us", C.c_double),
+                ("max_us", C.c_double), ("ci95_us", C.c_double), ("samples", C.c_int), ("reps", C.c_int)]
 
 
 class _Eval(C.Structure):
@@ -158,6 +163,7 @@ def _load() -> C.CDLL:
         "hf_image_free": (None, [vp]),
         "hf_run": (ip, [vp, vp, ip, vp, E]),
         "hf_time": (ip, [ip, vp, vp, vp, ip, ip, ip, ip, ip, vp, C.POINTER(_Timing), E]),
+        "hf_time_graph": (ip, [ip, vp, vp, vp, ip, ip, ip, ip, vp, C.POINTER(_GraphTiming), E]),
         "hf_profile": (ip, [cp, cp, ip, ip, ip, vp, ip, ip, ip, ip, ip, C.POINTER(_Eval), E]),
         "hf_search": (ip, [cp, cp, vp, C.POINTER(_SearchOpts), C.POINTER(ip), C.POINTER(ip), C.POINTER(ip),
                            C.POINTER(C.c_longlong), C.POINTER(vp), C.POINTER(vp), E]),
@@ -525,6 +531,16 @@ def time(mode: str, a: Module, b: Optional[Module], img: Image, grid_a: int = 0,
                         int(flush_l2), _stream(stream), C.byref(t), C.byref(err)), err)
     return {"median_us": t.median_us, "min_us": t.min_us, "mean_us": t.mean_us, "max_us": t.max_us,
             "reps": t.reps, "iqm_us": t.iqm_us}
+
+
+def time_graph(mode: str, a: Module, b: Optional[Module], img: Image, grid_a: int = 0, grid_b: int = 0,
+               reps: int = 20, samples: int = 7, stream=None) -> dict:
+    """Graph protocol (hf_time_graph): `reps` back-to-back repetitions captured as one CUDA graph,
+    launched `samples` times between consecutive events; per-repetition statistics over samples."""
+    t, err = _GraphTiming(), _Err()
+    _check(_lib.hf_time_graph(TIME_MODES[mode], a._h, b._h if b else None, img._h, grid_a, grid_b, reps, samples,
+                              _stream(stream), C.byref(t), C.byref(err)), err)
+    return {k: getattr(t, k) for k, _ in _GraphTiming._fields_}
 
 
 def profile(src1: str, src2: str, d1: int, d2: int, img: Image, regcap="off", grid: int = 0,

@@ -42,14 +42,27 @@ class Member:
 
 
 BN_SLOTS = 64  # >= grid / C + 2 for every grid the bench tries (C = 256: grids up to 15,872)
+GOLDEN = 0x9E3779B97F4A7C15
+M64 = (1 << 64) - 1
 
 
-def _bn(N: int, C: int, HW: int, slots: int = BN_SLOTS) -> Callable[[int], Workload]:
-    def make(seed: int = 0) -> Workload:
+def slice_seed(seed: int, offset: int) -> int:
+    """Seed of the stream that starts `offset` elements into the stream of `seed`.
+
+    A seeded array's element i is mix(seed + (i + 1) * golden) (memimage.cpp:26-29, 52-61),
+    so elements [offset, offset + n) of the array seeded `seed` are exactly the array of length
+    n seeded seed + offset * golden (mod 2^64). Batch shards are therefore bit-exact slices of
+    the whole-batch tensors with no image-format extension (the reference parser reads the
+    seed as uint64, memimage.cpp:135)."""
+    return (seed + offset * GOLDEN) & M64
+
+
+def _bn(N: int, C: int, HW: int, slots: int = BN_SLOTS) -> Callable[..., Workload]:
+    def make(seed: int = 0, offset: int = 0) -> Workload:
         n = N * C * HW
         # + the B200 form's grid-balancing workspace: BN_SLOTS partial (count, mean, M2) slots
         # per channel and one arrival counter per channel (zero between launches)
-        img = (f"array bn_x float32 {n} seed {1 + seed} uniform -1 1\n"
+        img = (f"array bn_x float32 {n} seed {slice_seed(1 + seed, offset)} uniform -1 1\n"
                f"array bn_stats float32 {2 * C} zero\n"
                f"array bn_pn int32 {slots * C} zero\narray bn_pa float32 {slots * C} zero\n"
                f"array bn_pm float32 {slots * C} zero\narray bn_cnt int32 {C} zero\n"
@@ -59,19 +72,19 @@ def _bn(N: int, C: int, HW: int, slots: int = BN_SLOTS) -> Callable[[int], Workl
     return make
 
 
-def _hist(n: int, lo: float = -4.0, hi: float = 4.0) -> Callable[[int], Workload]:
-    def make(seed: int = 0) -> Workload:
-        img = (f"array hi_x float32 {n} seed {2 + seed} uniform {lo:g} {hi:g}\n"
+def _hist(n: int, lo: float = -4.0, hi: float = 4.0) -> Callable[..., Workload]:
+    def make(seed: int = 0, offset: int = 0) -> Workload:
+        img = (f"array hi_x float32 {n} seed {slice_seed(2 + seed, offset)} uniform {lo:g} {hi:g}\n"
                f"array hi_out int32 64 zero\nscalar hi_n int32 {n}\n")
         return Workload(img, 4 * n + 4 * 64, f"hist 64 bins over [-4,4], {n} fp32", 4 * 64)
     return make
 
 
-def _maxpool(NC: int, H: int, W: int) -> Callable[[int], Workload]:
-    def make(seed: int = 0) -> Workload:
+def _maxpool(NC: int, H: int, W: int) -> Callable[..., Workload]:
+    def make(seed: int = 0, offset: int = 0) -> Workload:
         OH, OW = H // 2, W // 2
         n, m = NC * H * W, NC * OH * OW
-        img = (f"array mp_x float32 {n} seed {3 + seed} uniform -1 1\n"
+        img = (f"array mp_x float32 {n} seed {slice_seed(3 + seed, offset)} uniform -1 1\n"
                f"array mp_y float32 {m} zero\narray mp_idx int32 {m} zero\n"
                f"scalar mp_NC int32 {NC}\nscalar mp_H int32 {H}\nscalar mp_W int32 {W}\n"
                f"scalar mp_OH int32 {OH}\nscalar mp_OW int32 {OW}\n")
@@ -79,11 +92,11 @@ def _maxpool(NC: int, H: int, W: int) -> Callable[[int], Workload]:
     return make
 
 
-def _upsample(NC: int, IH: int, IW: int) -> Callable[[int], Workload]:
-    def make(seed: int = 0) -> Workload:
+def _upsample(NC: int, IH: int, IW: int) -> Callable[..., Workload]:
+    def make(seed: int = 0, offset: int = 0) -> Workload:
         OH, OW = 2 * IH, 2 * IW
         n, m = NC * IH * IW, NC * OH * OW
-        img = (f"array us_x float32 {n} seed {4 + seed} uniform -1 1\n"
+        img = (f"array us_x float32 {n} seed {slice_seed(4 + seed, offset)} uniform -1 1\n"
                f"array us_y float32 {m} zero\n"
                f"scalar us_NC int32 {NC}\nscalar us_IH int32 {IH}\nscalar us_IW int32 {IW}\n"
                f"scalar us_OH int32 {OH}\nscalar us_OW int32 {OW}\n")
@@ -91,10 +104,10 @@ def _upsample(NC: int, IH: int, IW: int) -> Callable[[int], Workload]:
     return make
 
 
-def _im2col(NC: int, H: int, W: int) -> Callable[[int], Workload]:
-    def make(seed: int = 0) -> Workload:
+def _im2col(NC: int, H: int, W: int) -> Callable[..., Workload]:
+    def make(seed: int = 0, offset: int = 0) -> Workload:
         n, m = NC * H * W, NC * 9 * H * W
-        img = (f"array ic_x float32 {n} seed {5 + seed} uniform -1 1\n"
+        img = (f"array ic_x float32 {n} seed {slice_seed(5 + seed, offset)} uniform -1 1\n"
                f"array ic_col float32 {m} zero\n"
                f"scalar ic_NC int32 {NC}\nscalar ic_H int32 {H}\nscalar ic_W int32 {W}\n")
         return Workload(img, 4 * n + 4 * m, f"im2col 3x3/p1 x[{NC},{H},{W}] fp32", 4 * m)
@@ -165,3 +178,21 @@ def scaled(key: str, factor: float, shape: str = "full", seed: int = 0) -> "tupl
     make, n0 = BATCHED[shape][key]
     n = max(1, int(round(n0 * factor)))
     return make(n)(seed), n
+
+
+def shard_offset(key: str, shape: str, rank: int, world: int) -> int:
+    """Element offset of rank's batch shard in member `key`'s seeded input tensor."""
+    make, n0 = BATCHED[shape][key]
+    if n0 % world:
+        raise ValueError(f"batch {n0} of {key} does not split over {world} ranks")
+    per_image = int(make(1)(0).image.split("\n")[0].split()[3])
+    return rank * (n0 // world) * per_image
+
+
+def shard(key: str, shape: str, rank: int, world: int) -> Workload:
+    """Rank `rank`'s batch shard (batch / world images) of member `key` at `shape`: the
+    contiguous slice of the whole-batch input tensor starting at shard_offset (the same values,
+    slice_seed), for the strong-scaling multi-GPU path. world = 1 is the
+    whole-batch workload, identical to MEMBERS[key].sizes[shape]()."""
+    make, n0 = BATCHED[shape][key]
+    return make(n0 // world)(0, shard_offset(key, shape, rank, world))

@@ -1,17 +1,30 @@
-"""Multi-GPU plumbing for the batch-sharded DL pairs.
+"""Multi-GPU plumbing for the batch-sharded DL pairs and the nonce-range-sharded crypto pairs
+(SURVEY.md §8e, C3/C5). Strong scaling: rank r of g owns batch images [r*N/g, (r+1)*N/g) of
+every member (pairs.shard: exact slices of the whole-batch tensors) and nonces
+[r*T/g, (r+1)*T/g) of a fixed range T.
 
-Each rank runs the fused pairs on its own batch shard; the only exchange is one reduction
-of the small outputs: histogram bins (int32 all-reduce sum, bit-exact) and the BatchNorm
-per-channel statistics (all-gather of (mean, var) per rank, merged in rank order with
-Chan's parallel formula — deterministic). Works with any torch.distributed backend
-(NCCL on the B200 box, gloo in the CPU tests)."""
+The fused kernels have no exchange step; the only collective of a step is ONE all-gather of a
+small packed buffer per rank, reduced identically on every rank:
+  * histogram bins: int32 sum (bit-exact, order-free);
+  * BatchNorm per-channel (mean, biased var) of each rank's shard: Chan's parallel merge in
+    rank order, in fp64 (deterministic; equals the whole-batch statistics within fp rounding);
+  * crypto: hit counts summed, winning nonce = MIN over ranks (sentinel = no hit).
+The reference is single-threaded by design and has no
+counterpart. Works with any torch.distributed backend (NCCL on the B200 box, gloo in the
+CPU tests); the merge runs with torch ops on whatever device the packed buffer lives on.
+"""
 from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Tuple
 
 import numpy as np
 
+NO_HIT = (1 << 63) - 1  # winning-nonce sentinel of a shard without a hit
+
 
 def merge_bn_stats(counts, means, variances):
-    """Chan et al. merge of per-shard (n, mean, biased var) -> (mean, biased var), in order."""
+    """Chan et al. merge of per-shard (n, mean, biased var) -> (mean, biased var), in order (numpy fp64)."""
     n = np.float64(0)
     mean = np.zeros_like(np.asarray(means[0], np.float64))
     m2 = np.zeros_like(mean)
@@ -26,17 +39,96 @@ def merge_bn_stats(counts, means, variances):
     return mean, m2 / n
 
 
-def reduce_outputs(dist, hist_bins=None, bn_stats=None, bn_count=None):
-    """The path's single collective step. hist_bins: int32 tensor (summed in place);
-    bn_stats: float32 tensor [2C] = (mean, var) pairs of this rank's shard. Returns the
-    merged (mean, var) as float64 numpy arrays when bn_stats is given."""
+def merge_bn_torch(counts, means, variances):
+    """merge_bn_stats with torch ops (same order, fp64): means/variances are [world, C]."""
     import torch
+    means = means.to(torch.float64)
+    variances = variances.to(torch.float64)
+    n = 0.0
+    mean = torch.zeros_like(means[0])
+    m2 = torch.zeros_like(mean)
+    for r, c in enumerate(counts):
+        c = float(c)
+        tot = n + c
+        delta = means[r] - mean
+        mean = mean + delta * (c / tot)
+        m2 = m2 + variances[r] * c + delta * delta * (n * c / tot)
+        n = tot
+    return mean, m2 / n
+
+
+@dataclass
+class Layout:
+    """Packed int32 cells of one rank's step outputs: (kind, tag, offset, cells, C)."""
+    slots: List[Tuple[str, str, int, int, int]] = field(default_factory=list)
+    cells: int = 0
+
+    def add(self, kind: str, tag: str, cells: int, channels: int = 0) -> int:
+        off = self.cells
+        self.slots.append((kind, tag, off, cells, channels))
+        self.cells += cells
+        return off
+
+
+def all_gather_packed(dist, packed):
+    """The step's single collective: every rank's packed int32 buffer -> [world, cells]."""
+    import torch
+    world = dist.get_world_size()
+    if dist.get_backend() == "nccl":
+        out = torch.empty((world, packed.numel()), dtype=packed.dtype, device=packed.device)
+        dist.all_gather_into_tensor(out, packed)
+        return out
+    parts = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(parts, packed)
+    return torch.stack(parts)
+
+
+def reduce_gathered(layout: Layout, gathered, bn_counts):
+    """Reduce [world, cells] gathered buffers: {tag: hist bins (int64 sum)} and
+    {tag: (mean, var) fp64 Chan merge over ranks in order}; bn_counts[r] = elements per channel
+    of rank r's shard."""
+    import torch
+    out = {}
+    for kind, tag, off, cells, ch in layout.slots:
+        block = gathered[:, off:off + cells]
+        if kind == "hist":
+            out[tag] = block.to(torch.int64).sum(0)
+        elif kind == "bn":
+            st = block.contiguous().view(torch.float32).reshape(block.shape[0], ch, 2)
+            out[tag] = merge_bn_torch(bn_counts, st[:, :, 0], st[:, :, 1])
+        elif kind == "crypto":  # (hits, winning nonce) pairs as int64 = 2 int32 cells each
+            v = block.contiguous().view(torch.int64).reshape(block.shape[0], -1, 2)
+            out[tag] = (v[:, :, 0].sum(0), v[:, :, 1].min(0).values)
+        else:
+            raise ValueError(kind)
+    return out
+
+
+def reduce_outputs(dist, hist_bins=None, bn_stats=None, bn_count=None):
+    """Single-pair convenience form: hist_bins int32 [64] (reduced in place), bn_stats float32
+    [2C] (mean, var) of this rank's shard -> merged (mean, var) as float64 numpy arrays."""
+    import torch
+    layout = Layout()
+    parts = []
     if hist_bins is not None:
-        dist.all_reduce(hist_bins)
+        layout.add("hist", "hist", hist_bins.numel())
+        parts.append(hist_bins.to(torch.int32).reshape(-1))
+    if bn_stats is not None:
+        layout.add("bn", "bn", bn_stats.numel(), bn_stats.numel() // 2)
+        parts.append(bn_stats.to(torch.float32).reshape(-1).view(torch.int32))
+    gathered = all_gather_packed(dist, torch.cat(parts))
+    red = reduce_gathered(layout, gathered, [bn_count] * dist.get_world_size())
+    if hist_bins is not None:
+        hist_bins.copy_(red["hist"].to(hist_bins.dtype))
     if bn_stats is None:
         return None
-    world = dist.get_world_size()
-    parts = [torch.empty_like(bn_stats) for _ in range(world)]
-    dist.all_gather(parts, bn_stats)
-    st = [p.cpu().numpy().astype(np.float64).reshape(-1, 2) for p in parts]
-    return merge_bn_stats([bn_count] * world, [s[:, 0] for s in st], [s[:, 1] for s in st])
+    m, v = red["bn"]
+    return m.cpu().numpy(), v.cpu().numpy()
+
+
+def nonce_slice(total: int, rank: int, world: int) -> Tuple[int, int]:
+    """(nonce0, count) of rank's contiguous slice of [0, total)."""
+    if total % world:
+        raise ValueError(f"nonce range {total} does not split over {world} ranks")
+    per = total // world
+    return rank * per, per
