@@ -185,6 +185,26 @@ int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regca
  * exactly L registers (HF_E_DEVICE otherwise: an undersized pool would block the .inc). */
 int hf_build_fused_regs(const char* src1, const char* src2, int d1, int d2, int regs1, int regs2,
                         int grid, const hf_image* specialize, hf_module** out, hf_error* err);
+/* hf_build_fused with every B200 option in one struct (zero-initialize, then set):
+ *   regcap          HF_REGCAP_OFF (-1), HF_REGCAP_AUTO (0) or an explicit cap;
+ *   regs1, regs2    per-interval register budgets as hf_build_fused_regs (regcap must be OFF);
+ *   vgrid1, vgrid2  dynamic interval scheduling: each interval runs its member as vgridN
+ *                   virtual blocks drawn from its own atomic queue (blockIdx.x / gridDim.x of the
+ *                   member = virtual block id / vgridN), so the launch grid becomes a persistent
+ *                   pool of CTAs and one member's long blocks no longer strand the other member's
+ *                   threads of the same CTA. Results equal the member launched with vgridN blocks.
+ *                   Needs structured members (no return/goto) and two free named barriers
+ *                   (HF_E_INVALID_ARGUMENT / HF_E_BARRIER_OVERFLOW); 0 = the static partition;
+ *   grid, min_blocks as hf_build_fused. B200-only; no reference analogue. */
+typedef struct hf_fuse_opts {
+  int regcap;
+  int regs1, regs2;
+  int vgrid1, vgrid2;
+  int grid;
+  int min_blocks;
+} hf_fuse_opts;
+int hf_build_fused_opts(const char* src1, const char* src2, int d1, int d2, const hf_fuse_opts* opts,
+                        const hf_image* specialize, hf_module** out, hf_error* err);
 /* One unfused kernel at its declared dims (regcap: HF_REGCAP_OFF = none, HF_REGCAP_AUTO = the
  * kernel's `//@ regcap=` annotation if present (the reference's exec.cpp:954), or a cap). */
 int hf_build_kernel(const char* src, int regcap, int grid, int min_blocks,

@@ -90,6 +90,26 @@ hf::rt::Module build_fused_regs(const char* s1, const char* s2, int d1, int d2, 
   return hf::rt::compile(hf::emit_sm100(r.fused, o), std::nullopt);
 }
 
+// sm_100a fused module with every B200 option: register cap or per-interval budgets, and
+// dynamic interval scheduling (virtual grids).
+hf::rt::Module build_fused_opts(const char* s1, const char* s2, int d1, int d2, const hf_fuse_opts& fo,
+                                const hf_image* spec) {
+  hf::SM sm = hf::rt::device_available() ? hf::rt::sm_from_device() : hf::SM::b200();
+  const bool budgets = fo.regs1 > 0 || fo.regs2 > 0;
+  if (budgets && fo.regcap != HF_REGCAP_OFF)
+    hf::raise(hf::Code::InvalidArgument, "a register cap and per-interval register budgets are exclusive");
+  hf::FuseResult r = hf::fuse_sources(s1, s2, d1, d2, regcap_spec(fo.regcap), sm, fo.grid);
+  if (fo.grid > 0) r.fused.grid = fo.grid;
+  hf::Sm100Options o;
+  o.min_blocks = fo.min_blocks;
+  o.regs1 = fo.regs1;
+  o.regs2 = fo.regs2;
+  o.vgrid1 = fo.vgrid1;
+  o.vgrid2 = fo.vgrid2;
+  o.specialize = scalars_of(spec);
+  return hf::rt::compile(hf::emit_sm100(r.fused, o), budgets ? std::nullopt : r.fused.cfg.reg_cap);
+}
+
 // sm_100a fused module; regcap AUTO means the register bound r0 with the B200 machine model.
 hf::rt::Module build_fused(const char* s1, const char* s2, int d1, int d2, int regcap, int grid, int min_blocks,
                            const hf_image* spec) {
@@ -208,6 +228,16 @@ int hf_build_fused(const char* src1, const char* src2, int d1, int d2, int regca
   return guarded(err, [&] {
     auto h = std::make_unique<hf_module>();
     h->m = build_fused(src1, src2, d1, d2, regcap, grid, min_blocks, specialize);
+    *out = h.release();
+  });
+}
+
+int hf_build_fused_opts(const char* src1, const char* src2, int d1, int d2, const hf_fuse_opts* opts,
+                        const hf_image* specialize, hf_module** out, hf_error* err) {
+  return guarded(err, [&] {
+    if (!opts) hf::raise(hf::Code::InvalidArgument, "hf_build_fused_opts: opts is NULL");
+    auto h = std::make_unique<hf_module>();
+    h->m = build_fused_opts(src1, src2, d1, d2, *opts, specialize);
     *out = h.release();
   });
 }

@@ -124,6 +124,15 @@ struct Sm100Options {
   // the two constituents no longer share one register count (the reference's single
   // reg_cap, machine.cpp:269-283). Needs warpgroup-aligned intervals (d1, d2 % 128 == 0).
   int regs1 = 0, regs2 = 0;
+  // Dynamic interval scheduling (fused kernels only; 0 = off, the reference's static
+  // partition). Each interval runs its member as `vgridN` VIRTUAL blocks drawn one at a time
+  // from its own atomic counter in the module (blockIdx.x / gridDim.x of the member become the
+  // virtual block id / vgridN), so a long-running block of one member no longer strands the
+  // other member's share of that CTA: the physical grid is persistent and each interval keeps
+  // pulling work until its own queue is empty. Preserves the semantics of the member launched
+  // with vgridN blocks (blocks are independent in CUDA); per virtual block the interval's
+  // locals and shared arrays start zeroed, as in the interpreter (exec.cpp:291).
+  int vgrid1 = 0, vgrid2 = 0;
 };
 
 struct Sm100Param {

@@ -38,7 +38,7 @@ TIME_MODES = {"single": 0, "sequential": 1, "two_stream": 2}
 EXPORTS = [
     "hf_free", "hf_version", "hf_fuse", "hf_fuse_report", "hf_normalize", "hf_check", "hf_lower",
     "hf_emit_kernel", "hf_register_bound", "hf_occupancy", "hf_device_count",
-    "hf_get_device_props", "hf_build_fused", "hf_build_fused_regs", "hf_build_kernel", "hf_build_naive", "hf_build_vertical",
+    "hf_get_device_props", "hf_build_fused", "hf_build_fused_opts", "hf_build_fused_regs", "hf_build_kernel", "hf_build_naive", "hf_build_vertical",
     "hf_module_get_info",
     "hf_module_source", "hf_module_entry", "hf_module_param", "hf_module_param_reads", "hf_module_barrier",
     "hf_module_cubin", "hf_launch", "hf_launch_ex", "hf_run_ex", "hf_module_free", "hf_image_parse", "hf_image_merge",
@@ -76,6 +76,11 @@ class _ModInfo(C.Structure):
                 ("regs", C.c_int), ("local_bytes", C.c_int), ("blocks_per_sm", C.c_int),
                 ("n_params", C.c_int), ("n_barriers", C.c_int), ("launch_regs", C.c_int),
                 ("interval_regs", C.c_int * 2)]
+
+
+class _FuseOpts(C.Structure):
+    _fields_ = [("regcap", C.c_int), ("regs1", C.c_int), ("regs2", C.c_int), ("vgrid1", C.c_int),
+                ("vgrid2", C.c_int), ("grid", C.c_int), ("min_blocks", C.c_int)]
 
 
 class _Timing(C.Structure):
@@ -130,6 +135,7 @@ def _load() -> C.CDLL:
         "hf_device_count": (ip, []),
         "hf_get_device_props": (ip, [C.POINTER(_Props), E]),
         "hf_build_fused": (ip, [cp, cp, ip, ip, ip, ip, ip, vp, C.POINTER(vp), E]),
+        "hf_build_fused_opts": (ip, [cp, cp, ip, ip, C.POINTER(_FuseOpts), vp, C.POINTER(vp), E]),
         "hf_build_fused_regs": (ip, [cp, cp, ip, ip, ip, ip, ip, vp, C.POINTER(vp), E]),
         "hf_build_kernel": (ip, [cp, ip, ip, ip, vp, C.POINTER(vp), E]),
         "hf_build_naive": (ip, [cp, cp, ip, ip, ip, C.POINTER(vp), E]),
@@ -414,6 +420,19 @@ class Module:
         h, err = C.c_void_p(), _Err()
         _check(_lib.hf_build_fused(src1.encode(), src2.encode(), d1, d2, _regcap(regcap), grid, min_blocks,
                                    specialize._h if specialize else None, C.byref(h), C.byref(err)), err)
+        return cls(h)
+
+    @classmethod
+    def fused_opts(cls, src1: str, src2: str, d1: int, d2: int, regcap="off", regs=None, vgrid=None,
+                   grid: int = 0, min_blocks: int = 0, specialize: Optional["Image"] = None) -> "Module":
+        """Every B200 option (hf_build_fused_opts): regcap, per-interval budgets regs=(r1, r2),
+        dynamic interval scheduling vgrid=(virtual grid of member 1, of member 2)."""
+        r1, r2 = regs or (0, 0)
+        v1, v2 = vgrid or (0, 0)
+        o = _FuseOpts(_regcap(regcap), r1, r2, v1, v2, grid, min_blocks)
+        h, err = C.c_void_p(), _Err()
+        _check(_lib.hf_build_fused_opts(src1.encode(), src2.encode(), d1, d2, C.byref(o),
+                                        specialize._h if specialize else None, C.byref(h), C.byref(err)), err)
         return cls(h)
 
     @classmethod
