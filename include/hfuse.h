@@ -165,6 +165,12 @@ int hf_register_bound(int regs1, int threads1, int regs2, int threads2, long lon
 int hf_occupancy(int regs, long long shmem, int threads, const char* sm_spec,
                  hf_occupancy_info* out, hf_error* err);
 
+/* combined_utilization (machine.cpp:285-289): the cycle-weighted
+ * utilization (u1*c1 + u2*c2) / (c1 + c2) of two kernels run back to back; `hfuse simulate
+ * --sequential` combines the members' device counters with it. Returns NaN when c1 or c2 <= 0
+ * (the reference throws InvalidArgument). */
+double hf_combined_utilization(double u1, long long c1, double u2, long long c2);
+
 /* ---- runtime (B200) --------------------------------------------------------------- */
 
 int hf_device_count(void);

@@ -13,6 +13,7 @@
 //   run      : run_functional of one kernel (exec.cpp:958-965)
 //   search   : search_config / fixed_partition_fuse with SimulatorBackend (search.cpp:124-175)
 //   regbound / occupancy : machine.cpp:236-283
+//   combine  : combined_utilization, machine.cpp:285-289
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -246,6 +247,14 @@ int cmd_occupancy(const Args& a) {
   return 0;
 }
 
+// combined_utilization (machine.cpp:285-289) on "u1 c1 u2 c2" arguments; %.17g output
+int cmd_combine(const Args& a) {
+  double v = combined_utilization(std::stod(a.pos.at(0)), std::stoll(a.pos.at(1)), std::stod(a.pos.at(2)),
+                                  std::stoll(a.pos.at(3)));
+  std::printf("%.17g\n", v);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -265,6 +274,7 @@ int main(int argc, char** argv) {
     if (cmd == "search") return cmd_search(a);
     if (cmd == "regbound") return cmd_regbound(a);
     if (cmd == "occupancy") return cmd_occupancy(a);
+    if (cmd == "combine") return cmd_combine(a);
     std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
     return 2;
   } catch (const Error& e) {

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -200,6 +201,11 @@ int hf_occupancy(int regs, long long shmem, int threads, const char* sm_spec, hf
     hf::Occupancy o = hf::occupancy(hf::Resources{regs, shmem, threads}, sm_of(sm_spec));
     *out = hf_occupancy_info{o.blocks_per_sm, int(o.limiting), o.warps, o.fraction};
   });
+}
+
+double hf_combined_utilization(double u1, long long c1, double u2, long long c2) {
+  if (c1 <= 0 || c2 <= 0) return std::nan("");
+  return hf::combined_utilization(u1, c1, u2, c2);
 }
 
 int hf_device_count(void) {

@@ -17,8 +17,13 @@
 // `simulate` and `search` run on the GPU: the reference's cycle simulator is replaced by
 // device execution (elapsed_us from CUDA events); `--sm` defaults to pascal-like for
 // `fuse`/`occupancy` (report parity) and to the live device for GPU commands.
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <filesystem>
 #include <fstream>
 #include <iostream>
@@ -38,6 +43,7 @@ struct Args {
   std::optional<uint64_t> seed;
   std::string sm = "pascal-like", regcap = "auto", style, out, trace, entry, profiler_cmd, dump, caps, iregs;
   bool sequential = false, sm_given = false, regcap_given = false, budgets = false;
+  bool launch_only = false, counters = true;
   int prefilter = 0;
   double prefilter_tol = -1.0;
   int d0 = 1024, d1 = 0, d2 = 0, regs = 0, threads = 0, granularity = 128, reps = 10, warmup = 3, grid = 0;
@@ -86,6 +92,8 @@ Args parse_args(int argc, char** argv) {
     else if (s == "--entry") a.entry = val();
     else if (s == "--dump-mem") a.dump = val();
     else if (s == "--sequential") a.sequential = true;
+    else if (s == "--launch-only") a.launch_only = true;  // internal: the ncu counter pass
+    else if (s == "--no-counters") a.counters = false;
     else if (s == "--budgets") a.budgets = true;
     else if (s == "--regs") a.regs = num();
     else if (s == "--shmem") a.shmem = std::stoll(val());
@@ -138,7 +146,7 @@ int cmd_fuse(const Args& a) {
     o.regs1 = r1;
     o.regs2 = r2;
     Sm100Kernel k = emit_sm100(r.fused, o);
-    write_text(path, k.source);
+    write_text(path, sm100_text(k, std::nullopt));
     r.fused.cfg.reg_cap = k.launch_regs;  // the report's occupancy: the pool per thread
     std::fputs(fuse_report(r).c_str(), stdout);
     std::printf("interval_regs = %d,%d (launch %d)\n", r1, r2, k.launch_regs);
@@ -151,16 +159,124 @@ int cmd_fuse(const Args& a) {
   return 0;
 }
 
-void print_run(double us, Image& img, const Args& a) {
-  std::printf("elapsed_us = %.3f\n", us);
-  std::printf("digest = %s\n", img.digest_hex().c_str());
-  if (!a.dump.empty()) write_text(a.dump, img.serialize());
+// ---- simulate on the device --------------------------------------------------------------
+// The reference prints run_timed's ProfileResult (exec.cpp:995-1007; --sequential adds
+// k1_cycles / k2_cycles and combines the rest with combined_utilization, mkfuse.cpp:180-196).
+// Here every key comes from a device measurement:
+//   *_cycles                 graph-timed mean launch time x the SM clock (cudaDevAttrClockRate)
+//   issue_slot_utilization   ncu smsp__issue_active (elapsed cycles, all schedulers)
+//   achieved_occupancy       ncu sm__warps_active (of the peak warps per SM, elapsed)
+//   meminst_stall_fraction   ncu (long_scoreboard + lg_throttle) / all stall reasons per issue
+//   spill_loads_stores       ncu local-memory load + store instructions executed
+// The ncu values come from one counter pass: the same command re-run under ncu with
+// --launch-only (each kernel launched once). Without ncu (or --no-counters) they print as nan.
+std::vector<std::string> g_argv;
+
+struct Counters {
+  double util = NAN, occ = NAN, mem = NAN;
+  long long spills = -1;
+};
+
+std::vector<std::string> csv_fields(const std::string& line) {
+  std::vector<std::string> out;
+  std::string cur;
+  bool q = false;
+  for (char ch : line) {
+    if (ch == '"') q = !q;
+    else if (ch == ',' && !q) {
+      out.push_back(cur);
+      cur.clear();
+    } else cur += ch;
+  }
+  out.push_back(cur);
+  return out;
+}
+
+std::string ncu_path() {
+  if (const char* e = std::getenv("HFUSE_NCU")) return e;
+  for (const char* p : {"/usr/local/cuda/bin/ncu", "/usr/bin/ncu"})
+    if (std::filesystem::exists(p)) return p;
+  return "";
+}
+
+std::vector<Counters> counter_pass() {
+  std::string ncu = ncu_path();
+  if (ncu.empty()) return {};
+  const char* metrics =
+      "smsp__issue_active.avg.pct_of_peak_sustained_elapsed,sm__warps_active.avg.pct_of_peak_sustained_elapsed,"
+      "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio,"
+      "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio,"
+      "smsp__average_warps_issue_stalled_selected_per_issue_active.ratio,"
+      "smsp__average_warps_active_per_issue_active.ratio,"
+      "smsp__sass_inst_executed_op_local_ld.sum,smsp__sass_inst_executed_op_local_st.sum";
+  std::string cmd = ncu + " --csv --clock-control none --metrics " + metrics + " " + std::filesystem::read_symlink("/proc/self/exe").string();
+  for (size_t i = 1; i < g_argv.size(); ++i) cmd += " '" + g_argv[i] + "'";
+  cmd += " --launch-only 2>/dev/null";
+  FILE* pipe = popen(cmd.c_str(), "r");
+  if (!pipe) return {};
+  std::vector<std::string> header;
+  std::vector<std::pair<std::string, std::map<std::string, double>>> rows;  // (ID, metrics) in order
+  char buf[4096];
+  while (std::fgets(buf, sizeof(buf), pipe)) {
+    std::string line(buf);
+    while (!line.empty() && (line.back() == '\n' || line.back() == '\r')) line.pop_back();
+    if (line.empty() || line[0] != '"') continue;
+    std::vector<std::string> f = csv_fields(line);
+    if (header.empty()) {
+      header = f;
+      continue;
+    }
+    auto col = [&](const char* name) -> std::string {
+      for (size_t i = 0; i < header.size() && i < f.size(); ++i)
+        if (header[i] == name) return f[i];
+      return "";
+    };
+    std::string kname = col("Kernel Name");
+    if (kname.rfind("fill_", 0) == 0 || kname.rfind("flush", 0) == 0 || kname.rfind("phase_spin", 0) == 0) continue;
+    std::string id = col("ID"), v = col("Metric Value");
+    v.erase(std::remove(v.begin(), v.end(), ','), v.end());
+    if (rows.empty() || rows.back().first != id) rows.push_back({id, {}});
+    rows.back().second[col("Metric Name")] = std::strtod(v.c_str(), nullptr);
+  }
+  if (pclose(pipe) != 0) return {};
+  std::vector<Counters> out;
+  for (auto& [id, m] : rows) {
+    Counters k;
+    auto get = [&](const char* n) { return m.count(n) ? m[n] : NAN; };
+    k.util = get("smsp__issue_active.avg.pct_of_peak_sustained_elapsed") / 100.0;
+    k.occ = get("sm__warps_active.avg.pct_of_peak_sustained_elapsed") / 100.0;
+    double stalled = get("smsp__average_warps_active_per_issue_active.ratio") -
+                     get("smsp__average_warps_issue_stalled_selected_per_issue_active.ratio");
+    k.mem = (get("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio") +
+             get("smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio")) /
+            stalled;
+    double sp = get("smsp__sass_inst_executed_op_local_ld.sum") + get("smsp__sass_inst_executed_op_local_st.sum");
+    k.spills = std::isnan(sp) ? -1 : (long long)sp;
+    out.push_back(k);
+  }
+  return out;
+}
+
+void print_profile(long long cycles, const Counters& k) {
+  // profile_report's keys and formats (exec.cpp:995-1007)
+  std::printf("elapsed_cycles = %lld\n", cycles);
+  std::printf("issue_slot_utilization = %.6f\n", k.util);
+  std::printf("meminst_stall_fraction = %.6f\n", k.mem);
+  std::printf("achieved_occupancy = %.6f\n", k.occ);
+  std::printf("spill_loads_stores = %lld\n", k.spills);
+}
+
+double combined(double u1, long long c1, double u2, long long c2) {
+  if (std::isnan(u1) || std::isnan(u2)) return NAN;
+  return combined_utilization(u1, c1, u2, c2);  // machine.cpp:285-289
 }
 
 int cmd_simulate(const Args& a) {
   if (!rt::device_available()) raise(Code::Device, "simulate runs on the GPU; no CUDA device is visible");
   Image img = images(a);
   rt::upload(img);
+  const double mhz = rt::props().clock_khz / 1000.0;
+  auto cycles = [&](double us) { return (long long)std::llround(us * mhz); };
   if (a.sequential) {
     need_inputs(a, 2);
     Loaded k1 = load_source(read_text(a.inputs[0])), k2 = load_source(read_text(a.inputs[1]));
@@ -169,15 +285,33 @@ int cmd_simulate(const Args& a) {
     // Parity run first (the timed repetitions mutate accumulating outputs).
     rt::launch(m1, img, a.grid);
     rt::launch(m2, img, a.grid);
+    if (a.launch_only) {
+      rt::synchronize();
+      return 0;
+    }
     rt::download(img);
     Image timing = images(a);
     rt::upload(timing);
-    rt::Timing t = rt::time(rt::Mode::Sequential, m1, &m2, timing, a.grid, a.grid, a.warmup, a.reps, true);
-    std::printf("k1_us = %.3f\n", rt::time(rt::Mode::Single, m1, nullptr, timing, a.grid, 0, a.warmup, a.reps, true).median_us);
-    std::printf("k2_us = %.3f\n", rt::time(rt::Mode::Single, m2, nullptr, timing, a.grid, 0, a.warmup, a.reps, true).median_us);
-    rt::Timing t2 = rt::time(rt::Mode::TwoStream, m1, &m2, timing, a.grid, a.grid, a.warmup, a.reps, true);
-    std::printf("two_stream_us = %.3f\n", t2.median_us);
-    print_run(t.median_us, img, a);
+    auto gt = [&](rt::Mode md, const rt::Module& x, const rt::Module* y) {
+      return rt::time_graph(md, x, y, timing, a.grid, a.grid, std::max(1, a.reps), 5).mean_us;
+    };
+    double t1 = gt(rt::Mode::Single, m1, nullptr), t2 = gt(rt::Mode::Single, m2, nullptr);
+    double tseq = gt(rt::Mode::Sequential, m1, &m2), two = gt(rt::Mode::TwoStream, m1, &m2);
+    std::vector<Counters> k = a.counters ? counter_pass() : std::vector<Counters>{};
+    Counters c1 = k.size() >= 2 ? k[0] : Counters{}, c2 = k.size() >= 2 ? k[1] : Counters{};
+    long long y1 = cycles(t1), y2 = cycles(t2);
+    Counters both;
+    both.util = combined(c1.util, y1, c2.util, y2);
+    both.mem = combined(c1.mem, y1, c2.mem, y2);
+    both.occ = combined(c1.occ, y1, c2.occ, y2);
+    both.spills = c1.spills < 0 || c2.spills < 0 ? -1 : c1.spills + c2.spills;
+    std::printf("k1_cycles = %lld\n", y1);
+    std::printf("k2_cycles = %lld\n", y2);
+    print_profile(y1 + y2, both);
+    std::printf("digest = %s\n", img.digest_hex().c_str());
+    // device extras: back to back and two-stream concurrent times of the same pair
+    std::printf("k1_us = %.3f\nk2_us = %.3f\nelapsed_us = %.3f\ntwo_stream_us = %.3f\n", t1, t2, tseq, two);
+    if (!a.dump.empty()) write_text(a.dump, img.serialize());
     return 0;
   }
   need_inputs(a, 1);
@@ -187,13 +321,19 @@ int cmd_simulate(const Args& a) {
   else if (a.regcap != "off") cap = std::stoi(a.regcap);
   rt::Module m = rt::compile(emit_sm100(k.kernel, k.prog.funcs), cap);
   rt::launch(m, img, a.grid);
+  if (a.launch_only) {
+    rt::synchronize();
+    return 0;
+  }
   rt::download(img);
   Image timing = images(a);
   rt::upload(timing);
-  rt::Timing t = rt::time(rt::Mode::Single, m, nullptr, timing, a.grid, 0, a.warmup, a.reps, true);
-  std::printf("registers = %d\n", m.regs);
-  std::printf("blocks_per_sm = %d\n", m.blocks_per_sm);
-  print_run(t.median_us, img, a);
+  double t = rt::time_graph(rt::Mode::Single, m, nullptr, timing, a.grid, 0, std::max(1, a.reps), 5).mean_us;
+  std::vector<Counters> ks = a.counters ? counter_pass() : std::vector<Counters>{};
+  print_profile(cycles(t), ks.empty() ? Counters{} : ks[0]);
+  std::printf("digest = %s\n", img.digest_hex().c_str());
+  std::printf("registers = %d\nblocks_per_sm = %d\nelapsed_us = %.3f\n", m.regs, m.blocks_per_sm, t);
+  if (!a.dump.empty()) write_text(a.dump, img.serialize());
   return 0;
 }
 
@@ -217,8 +357,10 @@ int cmd_search(const Args& a) {
   Image img;
   SM sm = a.sm_given ? SM::preset_or_file(a.sm) : SM::b200();
   if (!a.profiler_cmd.empty()) {
-    // budgets exist only in sm100 text, so a budget sweep hands the command sm100 candidates
-    be = std::make_unique<ExternalCommandBackend>(a.profiler_cmd, a.budgets ? Style::Sm100 : Style::Goto);
+    // budgets exist only in sm100 text, so a budget sweep (or --style sm100) hands the command
+    // sm100 candidates (manifest + __maxnreg__ cap; `hfuse profile` builds them as they are)
+    bool sm100 = a.budgets || a.style == "sm100";
+    be = std::make_unique<ExternalCommandBackend>(a.profiler_cmd, sm100 ? Style::Sm100 : Style::Goto);
   } else {
     if (!rt::device_available()) raise(Code::Device, "search times candidates on the GPU; no CUDA device is visible");
     if (!a.sm_given) sm = rt::sm_from_device();
@@ -283,6 +425,10 @@ int cmd_profile(const Args& a) {
     Sm100Options o;
     for (const auto& [n, s] : img.scalars) o.specialize[n] = ScalarVal{s.ty, s.i, s.f};
     k = emit_sm100(l.kernel, l.prog.funcs, o);
+  } else if (is_sm100_text(text)) {
+    // an sm100 candidate (search --style sm100 --profiler-cmd): the cap is already in the code
+    k = parse_sm100_text(text, a.grid);
+    cap.reset();
   } else {
     k = wrap_goto(text, a.grid);
   }
@@ -348,6 +494,7 @@ int cmd_emit(const Args& a) {
 
 int main(int argc, char** argv) {
   try {
+    g_argv.assign(argv, argv + argc);
     Args a = parse_args(argc, argv);
     if (a.cmd == "fuse") return cmd_fuse(a);
     if (a.cmd == "simulate") return cmd_simulate(a);

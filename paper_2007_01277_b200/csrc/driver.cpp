@@ -121,15 +121,69 @@ Sm100Kernel wrap_goto(const std::string& text, int grid) {
   return k;
 }
 
+// Exported sm_100a text: the register cap is part of the code (__maxnreg__ replaces the launch
+// bounds -- nvcc ignores --maxrregcount for a kernel that carries __launch_bounds__), and a
+// first-line manifest lets `hfuse profile` rebuild the launch metadata from the file alone:
+//   // hfuse-sm100 entry=E threads=T smem=S launch_regs=L params=name:af,name:si,...
+// (a = array, s = scalar; f = float, i = int).
+std::string sm100_text(const Sm100Kernel& k, std::optional<int> cap) {
+  std::string s = k.source;
+  if (cap) {
+    size_t at = s.find("__launch_bounds__(");
+    if (at != std::string::npos) s.replace(at, s.find(')', at) - at + 1, "__maxnreg__(" + std::to_string(*cap) + ")");
+  }
+  std::string m = "// hfuse-sm100 entry=" + k.entry + " threads=" + std::to_string(k.threads) +
+                  " smem=" + std::to_string(k.smem_bytes) + " launch_regs=" + std::to_string(k.launch_regs) +
+                  " params=";
+  for (size_t i = 0; i < k.params.size(); ++i) {
+    const Sm100Param& p = k.params[i];
+    if (p.specialized) raise(Code::InvalidArgument, "exported sm100 text cannot carry specialized scalars");
+    m += (i ? "," : "") + p.name + ":" + (p.array ? "a" : "s") + (p.ty == Ty::Float ? "f" : "i");
+  }
+  return m + "\n" + s;
+}
+
+bool is_sm100_text(const std::string& text) { return text.rfind("// hfuse-sm100 ", 0) == 0; }
+
+// The inverse of sm100_text's manifest (the code itself is compiled as written).
+Sm100Kernel parse_sm100_text(const std::string& text, int grid) {
+  if (!is_sm100_text(text)) raise(Code::InvalidArgument, "not an hfuse sm100 candidate (no manifest line)");
+  std::stringstream line(text.substr(0, text.find('\n')));
+  Sm100Kernel k;
+  std::string tok;
+  line >> tok >> tok;  // "//", "hfuse-sm100"
+  while (line >> tok) {
+    size_t eq = tok.find('=');
+    if (eq == std::string::npos) continue;
+    std::string key = tok.substr(0, eq), v = tok.substr(eq + 1);
+    if (key == "entry") k.entry = v;
+    else if (key == "threads") k.threads = std::stoi(v);
+    else if (key == "smem") k.smem_bytes = std::stoll(v);
+    else if (key == "launch_regs") k.launch_regs = std::stoi(v);
+    else if (key == "params") {
+      std::stringstream ps(v);
+      std::string item;
+      while (std::getline(ps, item, ',')) {
+        size_t colon = item.find(':');
+        if (colon == std::string::npos || item.size() != colon + 3)
+          raise(Code::InvalidArgument, "bad parameter '" + item + "' in the sm100 manifest");
+        bool array = item[colon + 1] == 'a';
+        Ty ty = item[colon + 2] == 'f' ? Ty::Float : Ty::Int;
+        k.params.push_back(Sm100Param{item.substr(0, colon), ty, array, array, false, {}, array});
+      }
+    }
+  }
+  if (k.entry.empty() || k.threads <= 0) raise(Code::InvalidArgument, "incomplete sm100 manifest");
+  k.grid = grid > 0 ? grid : 1;
+  k.source = text;
+  return k;
+}
+
 std::string emit(const Fused& f, Style style) {
   switch (style) {
     case Style::Structured: return emit_structured(f);
     case Style::Goto: return emit_goto(f);
-    case Style::Sm100: {
-      std::string s = emit_sm100(f).source;
-      if (f.cfg.reg_cap) s = "// hfuse: compile with --maxrregcount=" + std::to_string(*f.cfg.reg_cap) + "\n" + s;
-      return s;
-    }
+    case Style::Sm100: return sm100_text(emit_sm100(f), f.cfg.reg_cap);
   }
   return {};
 }

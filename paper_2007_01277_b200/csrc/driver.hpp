@@ -31,5 +31,9 @@ std::string fuse_report(const FuseResult& r);
 std::string emit(const Fused& f, Style style);
 std::string read_text(const std::string& path);
 Sm100Kernel wrap_goto(const std::string& goto_text, int grid);
+// Exported sm_100a candidate text (register cap as __maxnreg__, manifest first line) and back.
+std::string sm100_text(const Sm100Kernel& k, std::optional<int> cap);
+bool is_sm100_text(const std::string& text);
+Sm100Kernel parse_sm100_text(const std::string& text, int grid);
 
 }  // namespace hf

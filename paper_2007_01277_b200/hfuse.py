@@ -37,7 +37,7 @@ TIME_MODES = {"single": 0, "sequential": 1, "two_stream": 2}
 # Every symbol include/hfuse.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "hf_free", "hf_version", "hf_fuse", "hf_fuse_report", "hf_normalize", "hf_check", "hf_lower",
-    "hf_emit_kernel", "hf_register_bound", "hf_occupancy", "hf_device_count",
+    "hf_emit_kernel", "hf_register_bound", "hf_occupancy", "hf_combined_utilization", "hf_device_count",
     "hf_get_device_props", "hf_build_fused", "hf_build_fused_opts", "hf_build_fused_regs", "hf_build_kernel", "hf_build_naive", "hf_build_vertical",
     "hf_module_get_info",
     "hf_module_source", "hf_module_entry", "hf_module_param", "hf_module_param_reads", "hf_module_barrier",
@@ -132,6 +132,7 @@ def _load() -> C.CDLL:
         "hf_emit_kernel": (ip, [cp, ip, C.POINTER(vp), E]),
         "hf_register_bound": (ip, [ip, ip, ip, ip, C.c_longlong, cp, C.POINTER(ip), E]),
         "hf_occupancy": (ip, [ip, C.c_longlong, ip, cp, C.POINTER(_Occ), E]),
+        "hf_combined_utilization": (C.c_double, [C.c_double, C.c_longlong, C.c_double, C.c_longlong]),
         "hf_device_count": (ip, []),
         "hf_get_device_props": (ip, [C.POINTER(_Props), E]),
         "hf_build_fused": (ip, [cp, cp, ip, ip, ip, ip, ip, vp, C.POINTER(vp), E]),
@@ -269,6 +270,11 @@ def register_bound(regs1: int, threads1: int, regs2: int, threads2: int, fused_s
     _check(_lib.hf_register_bound(regs1, threads1, regs2, threads2, fused_shmem, _b(sm), C.byref(out),
                                   C.byref(err)), err)
     return out.value
+
+
+def combined_utilization(u1: float, c1: int, u2: float, c2: int) -> float:
+    """machine.cpp:285-289: cycle-weighted utilization of two kernels run back to back."""
+    return _lib.hf_combined_utilization(u1, c1, u2, c2)
 
 
 LIMITS = ["registers", "shared_memory", "threads", "block_slots"]

@@ -117,3 +117,19 @@ def test_prefilter_needs_a_measuring_backend(corpus, tmp_path):
     r = run("search", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--profiler-cmd", "echo 11",
             "--prefilter", 2)
     assert r.returncode == 0 and "evaluated = 14" in r.stdout
+
+
+def test_sm100_export_carries_cap_and_manifest(corpus, tmp_path):
+    """`fuse --style sm100 --regcap 32`: the cap is in the code as __maxnreg__(32) (nvcc ignores
+    --maxrregcount under __launch_bounds__) and the first line is the manifest `hfuse profile`
+    rebuilds the launch from (the exported text used to drop the cap)."""
+    for stem in ("batchnorm", "histogram"):
+        (tmp_path / f"{stem}.mk").write_text(corpus["kernels"][stem])
+    out = tmp_path / "f.cu"
+    r = subprocess.run([EXE, "fuse", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--d1", "896", "--d2",
+                        "128", "--style", "sm100", "--regcap", "32", "-o", out], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    text = out.read_text()
+    first = text.splitlines()[0]
+    assert first.startswith("// hfuse-sm100 entry=fused_batchnorm_histogram threads=1024 ")
+    assert "params=" in first and "__maxnreg__(32)" in text and "__launch_bounds__" not in text

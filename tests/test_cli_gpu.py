@@ -32,6 +32,16 @@ def test_simulate_sequential_digest_matches_reference(gpu, corpus, tmp_path):
     kv = dict(line.split(" = ") for line in r.stdout.strip().splitlines())
     assert kv["digest"] == rec["seeds"]["3"]["sequential"]
     assert float(kv["elapsed_us"]) > 0
+    # the reference's keys, in its order (mkfuse.cpp:190-196 + exec.cpp:995-1007), from device
+    # measurements: cycles from the graph-timed member launches, counters from one ncu pass
+    keys = [line.split(" = ")[0] for line in r.stdout.strip().splitlines()]
+    assert keys[:8] == ["k1_cycles", "k2_cycles", "elapsed_cycles", "issue_slot_utilization",
+                        "meminst_stall_fraction", "achieved_occupancy", "spill_loads_stores", "digest"]
+    c1, c2 = int(kv["k1_cycles"]), int(kv["k2_cycles"])
+    assert c1 > 0 and c2 > 0 and int(kv["elapsed_cycles"]) == c1 + c2
+    u = float(kv["issue_slot_utilization"])
+    assert 0.0 < u < 1.0 and 0.0 < float(kv["achieved_occupancy"]) <= 1.0
+    assert 0.0 <= float(kv["meminst_stall_fraction"]) <= 1.0 and int(kv["spill_loads_stores"]) == 0
 
 
 @pytest.mark.gpu
@@ -84,3 +94,18 @@ def test_search_with_model_prefilter(gpu, corpus, tmp_path):
     res = hf.search(corpus["kernels"]["batchnorm"], corpus["kernels"]["histogram"], img, reps=3, prefilter=2,
                     prefilter_tol=0.0)
     assert sorted(res["model"]) == [128, 256, 384, 512, 640, 768, 896] and len(res["trace"]) == 4
+
+
+@pytest.mark.gpu
+def test_profile_command_with_sm100_candidates(gpu, corpus, tmp_path):
+    """`search --style sm100 --profiler-cmd 'hfuse profile ...'`: the command receives sm100
+    candidates (manifest + the register cap as __maxnreg__) and times each on the device; the
+    fold picks a point of the same 14-row sweep."""
+    write_corpus(corpus, tmp_path)
+    trace = tmp_path / "t.csv"
+    cmd = f"{EXE} profile --mem {tmp_path / 'batchnorm.img'} --mem {tmp_path / 'histogram.img'} --reps 3"
+    r = run("search", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--style", "sm100",
+            "--profiler-cmd", cmd, "--trace", trace, "-o", tmp_path / "best.cu")
+    assert r.returncode == 0, r.stderr
+    rows = trace.read_text().splitlines()
+    assert len(rows) == 15 and all(int(row.split(",")[3]) > 0 for row in rows[1:])

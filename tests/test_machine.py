@@ -35,3 +35,18 @@ def test_does_not_fit(hf):
     with pytest.raises(hf.HFuseError) as e:
         hf.occupancy(255, 0, 1024)
     assert e.value.name == "DoesNotFit"
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+@pytest.mark.parametrize("case", [(0.5, 100, 0.25, 300), (0.2307, 2788, 0.1672, 8212), (1.0, 1, 0.0, 10**12),
+                                  (0.123456789, 987654321, 0.987654321, 123456789)])
+def test_combined_utilization_matches_reference(hf, case):
+    """hf_combined_utilization (include/hfuse.h) == the reference's machine.cpp:285-289."""
+    import subprocess
+    out = subprocess.run([oracle.REF, "combine", *map(str, case)], capture_output=True, text=True, check=True)
+    assert hf.combined_utilization(*case) == float(out.stdout)
+
+
+def test_combined_utilization_rejects_empty_kernels(hf):
+    import math
+    assert math.isnan(hf.combined_utilization(0.5, 0, 0.5, 10))
