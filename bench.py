@@ -331,18 +331,27 @@ def best_two_stream(hf, ka, kb, img, ga, gb, grids, stream, reps, samples):
     return best
 
 
-def search_pair(hf, sa, sb, img, d0s, grids, stream, args):
+def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3):
     """Device split search over block size d0 x launch grid (search_config per grid, steady
-    graph protocol). Returns (best search result, grid, compact trace)."""
-    best, grid, trace = None, None, []
+    graph protocol), then the `top` fastest distinct points re-timed with a longer graph (the
+    minimum of a few hundred short samples is biased low; the re-timing picks on equal terms).
+    Returns (config dict, compact trace)."""
+    trace = []
     for d0 in d0s:
         for g in grids if d0 == 1024 else [2 * x for x in grids]:
             rg = hf.search(sa, sb, img, d0=d0, grid=g, reps=args.search_reps, warmup=1, specialize=True,
                            flush_l2=False, granularity=args.granularity)
             trace += [(d0, g, t["d1"], t["reg_cap"], round(t["us"], 2)) for t in rg["trace"]]
-            if best is None or rg["best_time"] < best["best_time"]:
-                best, grid = rg, g
-    return best, grid, trace
+    best = None
+    for d0, g, d1, cap, _ in sorted(trace, key=lambda t: t[4])[:top]:
+        cfg = {"d1": d1, "d2": d0 - d1, "reg_cap": None if cap in ("none", None) else int(cap),
+               "interval_regs": None, "grid": g}
+        m = build_fused(hf, sa, sb, cfg, img)
+        t = gtime(hf, "single", m, None, img, g, 0, stream, 10, 5)["mean_us"]
+        if best is None or t < best[1]:
+            best = (cfg, t)
+        del m
+    return best[0], trace
 
 
 def build_fused(hf, sa, sb, cfg, img):
@@ -437,9 +446,8 @@ def main():
             mgrid[k] = min(ts, key=ts.get)
         cfgs, traces = [], {}
         for i, (a, b) in enumerate(pair_list):
-            r, g, trace = search_pair(hf, src[a], src[b], imgs[i], d0s, grids, stream, args)
-            cfgs.append({"d1": r["d1"], "d2": r["d2"], "reg_cap": r["reg_cap"], "interval_regs": r["interval_regs"],
-                         "grid": g})
+            cfg, trace = search_pair(hf, src[a], src[b], imgs[i], d0s, grids, stream, args)
+            cfgs.append(cfg)
             traces[f"{a}+{b}"] = trace
         plan = {"mgrid": mgrid, "cfgs": cfgs, "traces": traces}
     plan = D.bcast(plan)
@@ -490,10 +498,10 @@ def main():
     for i, (a, b) in enumerate(pair_list):
         for k in (a, b):
             if k == "hist":
-                copies.append((i, "hi_out", layout.add("hist", f"{i}", 64), 64))
+                copies.append((i, "hi_out", layout.add("hist", f"{i}:hist", 64), 64))
             elif k == "bn":
                 C = int(work["bn"].image.split("scalar bn_C int32 ")[1].split()[0])
-                copies.append((i, "bn_stats", layout.add("bn", f"{i}", 2 * C, C), 2 * C))
+                copies.append((i, "bn_stats", layout.add("bn", f"{i}:bn", 2 * C, C), 2 * C))
     packed = torch.zeros(max(1, layout.cells), dtype=torch.int32, device="cuda")
     bn_count = None
     if "bn" in keys:
@@ -663,11 +671,10 @@ def main():
         "vs_baseline": None,
         "dtype": "fp32/int32",
         "data": "synthetic (splitmix64-seeded in HBM)",
-        "config": {"workload": ("C2: 10 DL pairs of BN-stats/Hist 64x256x56x56, Im2Col 32x64x56x56, "
-                                "MaxPool 64x64x112x112, Upsample 64x256x28x28" if shape == "full" else
-                                "C5 conv3_x shapes: 10 DL pairs") + f", batch/{sworld} per GPU, searched splits",
-                   "l2": "own tensors per pair, >=260MB each > L2; no flush",
-                   "timing": f"step: K steps 1 event pair; pairs: CUDA graph {R} reps x {S} samples",
+        "config": {"workload": ("C2 10 DL pairs: BN,Hist 64x256x56x56 Im2Col 32x64x56x56 MaxPool 64x64x112x112 "
+                                "Upsample 64x256x28x28" if shape == "full" else "C5 conv3_x: 10 DL pairs")
+                               + f"; batch/{sworld} per GPU",
+                   "l2": "per-pair tensors >260MB>L2, no flush",
                    "parallelism": f"dp{world} batch shards" if args.scaling == "strong" else f"{world} replicas"},
         "speedup_geomean": round(geo, 4),
         "step_speedup": round(min(unfused_us, unfused_ov_us) / us_per_step, 4),
@@ -686,6 +693,9 @@ def main():
         "clocks": {k: clk.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         "cpu_baseline": cpu,
     }
+    if parity and parity.get("merged_bn"):
+        mb = parity["merged_bn"]
+        line["merged_bn"] = {"ok": mb["ok"], "max_rel_err": max(v for k, v in mb.items() if k != "ok")}
     if crypto_res:
         # pair -> [fused us, min(seq, two-stream) us, speed-up, roofline fraction]
         line["crypto"] = {c["pair"]: [round(c["fused_us"], 1), round(min(c["seq_us"], c["two_stream_us"]), 1),
@@ -694,10 +704,16 @@ def main():
                           for c in crypto_res["pairs"]}
         line["crypto_parity"] = crypto_res["parity_ok"]
     text = json.dumps(line, separators=(",", ":"), ensure_ascii=False)
-    if len(text.encode()) > LINE_LIMIT:  # keep the headline parseable: drop the least essential keys
-        for k in ("crypto_parity", "unfused_step_us"):
-            line.pop(k, None)
-        line["config"].pop("timing", None)
+    for drop in ("unfused_step_us", "crypto_parity"):  # keep the headline parseable
+        if len(text.encode()) <= LINE_LIMIT:
+            break
+        line.pop(drop, None)
+        text = json.dumps(line, separators=(",", ":"), ensure_ascii=False)
+    if len(text.encode()) > LINE_LIMIT:
+        line["roofline"].pop("peak_source", None)
+        text = json.dumps(line, separators=(",", ":"), ensure_ascii=False)
+    if len(text.encode()) > LINE_LIMIT and line.get("cpu_baseline"):
+        line["cpu_baseline"].pop("sample", None)
         text = json.dumps(line, separators=(",", ":"), ensure_ascii=False)
     print(text, flush=True)
     D.close()
@@ -745,6 +761,10 @@ def check_merged_bn(P, shape, merged, layout, rank):
 # ---------------------------------------------------------------------------------------
 
 CRYPTO_COUNTS = {"sha256d": 1 << 24, "blake2b": 1 << 23, "blake256": 1 << 24, "ethash": 1 << 20}
+# the paper's six crypto pairs (every pair of its four hashes; the tunable
+# Ethash always second, so its interval takes d0 - 512)
+CRYPTO_PAIRS = [("sha256d", "blake2b"), ("blake256", "ethash"), ("sha256d", "blake256"),
+                ("sha256d", "ethash"), ("blake256", "blake2b"), ("blake2b", "ethash")]
 ETHASH_PAGES = 1 << 25  # 4 GiB synthetic DAG (>> the 126 MB L2)
 
 
@@ -805,7 +825,7 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
     cgrids = [296, 592]
     srcs = {k: open(os.path.join(P.KERNELS, "b200", k + ".mk")).read() for k in CR.MEMBERS}
     out = {"pairs": [], "parity_ok": True}
-    for a, b in (("sha256d", "blake2b"), ("blake256", "ethash")):
+    for a, b in CRYPTO_PAIRS:
         na0, na = SH.nonce_slice(CRYPTO_COUNTS[a], rank, world)
         nb0, nb = SH.nonce_slice(CRYPTO_COUNTS[b], rank, world)
         gmax = max(cgrids)
@@ -947,9 +967,8 @@ def ratio_study(hf, P, pair_list, src, shape, grids, d0s, stream, args):
                 ts = {g: gtime(hf, "single", k, None, img, g, 0, stream, 5, 3)["mean_us"] for g in grids}
                 g = min(ts, key=ts.get)
                 alone[name] = (g, ts[g])
-            best, grid, _ = search_pair(hf, src[a], src[b], img, d0s, grids, stream, args)
-            cfg = {"d1": best["d1"], "d2": best["d2"], "reg_cap": best["reg_cap"], "interval_regs": None,
-                   "grid": grid}
+            cfg, _ = search_pair(hf, src[a], src[b], img, d0s, grids, stream, args)
+            grid = cfg["grid"]
             m = build_fused(hf, src[a], src[b], cfg, img)
             tf = gtime(hf, "single", m, None, img, grid, 0, stream, args.reps, 5)["mean_us"]
             (ga, ta), (gb, tb) = alone[a], alone[b]

@@ -1,0 +1,57 @@
+"""The reference-side binding proven: integration/b200_backend.cpp is the
+INTEGRATION.md §3 `B200Backend` compiled against the unmodified reference headers and library
+(oracle/Makefile `binding`) plus libhfuse.so. The reference's own search_config drives it -- and,
+in the same program, the reference's ExternalCommandBackend with `hfuse profile` as the
+command -- over corpus BatchNorm + Hist; both sweeps must be the reference's 14 points, and the
+split each picks must be as fast, in hfuse's own device search, as hfuse's pick (timing noise
+at these microsecond kernel times can swap near-equal points)."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+BIN = os.path.join(ROOT, "oracle", "_ref", "b200_backend")
+EXE = os.path.join(ROOT, "paper_2007_01277_b200", "bin", "hfuse")
+
+
+def sections(out):
+    res, cur = {}, None
+    for line in out.splitlines():
+        if line.startswith("["):
+            cur = line.strip("[]")
+            res[cur] = {"kv": {}, "rows": []}
+        elif " = " in line:
+            k, v = line.split(" = ")
+            res[cur]["kv"][k] = v
+        elif line and not line.startswith("d1,"):
+            res[cur]["rows"].append(line.split(","))
+    return res
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(BIN), reason="binding not built (needs /root/reference at build time)")
+def test_reference_search_config_drives_b200(gpu, corpus, tmp_path):
+    hf = gpu
+    for stem in ("batchnorm", "histogram"):
+        (tmp_path / f"{stem}.mk").write_text(corpus["kernels"][stem])
+        (tmp_path / f"{stem}.img").write_text(corpus["images"][stem])
+    cmd = f"{EXE} profile --mem {tmp_path / 'batchnorm.img'} --mem {tmp_path / 'histogram.img'} --reps 5"
+    r = subprocess.run([BIN, tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", tmp_path / "batchnorm.img",
+                        tmp_path / "histogram.img", "--cmd", cmd], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr
+    s = sections(r.stdout)
+    img = hf.Image(corpus["images"]["batchnorm"]).merge(hf.Image(corpus["images"]["histogram"])).upload()
+    ours = hf.search(corpus["kernels"]["batchnorm"], corpus["kernels"]["histogram"], img, reps=10, specialize=True)
+    us = {}  # d1 -> hfuse's best time over its caps (r0 comes from ptxas there, from the model here)
+    for row in ours["trace"]:
+        us[row["d1"]] = min(us.get(row["d1"], float("inf")), row["us"])
+    best = min(us.values())
+    for tag in ("B200Backend", "ExternalCommandBackend"):
+        kv, rows = s[tag]["kv"], s[tag]["rows"]
+        assert kv["evaluated"] == "14" and len(rows) == 14
+        assert all(int(row[3]) > 0 for row in rows)
+        d1 = int(kv["best_d1"])
+        assert int(kv["best_d2"]) == 1024 - d1
+        assert d1 in us and us[d1] <= 1.15 * best, (tag, d1, us, best)

@@ -44,7 +44,9 @@ def test_dynamic_interval_scheduling_matches_oracle(gpu, a, b, vgrid):
         m = hf.Module.fused_opts(sa, sb, 256, 256, vgrid=vgrid, grid=grid, specialize=img)
         assert "hf_sched" in m.source
         for launch in range(3):
-            img.upload()
+            # a fresh image per launch (re-uploading a downloaded image re-sends its contents,
+            # which would accumulate the histogram)
+            img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
             m.run(img, grid)
             img.download()
             for key, w in ((a, wa), (b, wb)):
