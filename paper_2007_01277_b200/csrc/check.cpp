@@ -320,6 +320,17 @@ class Checker {
         call_args(*f, s.val, s.pos);
         break;
       }
+      case SK::AsyncCopy: {
+        Pos pos = s.name_pos.valid() ? s.name_pos : s.pos;
+        const Sym& g = need(s.name, pos);
+        const Sym& sh = need(s.outs[0], s.pos);
+        if (g.kind != Sym::ArrayParam || sh.kind != Sym::SharedArray)
+          raise(Code::TypeMismatch, "async_copy copies a global array into a shared array", s.pos);
+        if (type(s.idx[0]) != Ty::Int || type(s.val[0]) != Ty::Int)
+          raise(Code::TypeMismatch, "async_copy indices must be int", s.pos);
+        if (g.ty != sh.ty) raise(Code::TypeMismatch, "async_copy arrays differ in element type", s.pos);
+        break;
+      }
       case SK::VLoad:
       case SK::VStore: {
         Pos pos = s.name_pos.valid() ? s.name_pos : s.pos;

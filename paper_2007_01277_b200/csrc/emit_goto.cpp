@@ -182,6 +182,8 @@ struct GotoPrinter {
         break;
       case SK::VLoad:
       case SK::VStore:
+      case SK::AsyncCopy:
+      case SK::AsyncWait:
         // MK+ statements have no reference spelling; expand them element-wise so the
         // naive text stays plain CUDA.
         raise(Code::InvalidArgument,

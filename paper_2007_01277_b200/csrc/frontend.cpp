@@ -596,8 +596,29 @@ class Parser {
             want(T::Semi);
             return s;
           }
-          if ((at_ident("fence") || at_ident("warp_sync")) && at(T::LParen, 1) && at(T::RParen, 2)) {
-            s.k = next().text == "fence" ? SK::Fence : SK::WarpSync;
+          if (at_ident("async_copy") && at(T::LParen, 1)) {
+            // async_copy(sarr, j, garr, i): 16-byte asynchronous global -> shared copy
+            next();
+            want(T::LParen);
+            s.k = SK::AsyncCopy;
+            Tok sa = want(T::Ident);
+            s.outs.push_back(sa.text);
+            want(T::Comma);
+            s.val.push_back(expr());
+            want(T::Comma);
+            Tok ga = want(T::Ident);
+            s.name = ga.text;
+            s.name_pos = ga.pos;
+            want(T::Comma);
+            s.idx.push_back(expr());
+            want(T::RParen);
+            want(T::Semi);
+            return s;
+          }
+          if ((at_ident("fence") || at_ident("warp_sync") || at_ident("async_wait")) && at(T::LParen, 1) &&
+              at(T::RParen, 2)) {
+            const std::string w = next().text;
+            s.k = w == "fence" ? SK::Fence : w == "warp_sync" ? SK::WarpSync : SK::AsyncWait;
             next();
             next();
             want(T::Semi);

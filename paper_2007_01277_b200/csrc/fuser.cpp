@@ -455,6 +455,10 @@ struct Liveness {
         expr(s.idx[0]);
         for (const auto& d : s.outs) touch(find(d));
         break;
+      case SK::AsyncCopy:
+        expr(s.idx[0]);
+        expr(s.val[0]);
+        break;
       case SK::If:
         expr(s.val[0]);
         block(s.body);

@@ -289,6 +289,7 @@ bool uses_extensions(const Kernel& k) {
   bool ext = false;
   walk(k.body, [&](const Stmt& s) {
     if (s.k == SK::VLoad || s.k == SK::VStore || s.k == SK::Fence || s.k == SK::WarpSync ||
+        s.k == SK::AsyncCopy || s.k == SK::AsyncWait ||
         (s.k == SK::For && s.unroll != 0))
       ext = true;
     exprs_of(s, [&](const Expr& e) {
@@ -502,6 +503,18 @@ struct MkPrinter {
       case SK::WarpSync:
         pad(ind);
         o += "warp_sync();\n";
+        break;
+      case SK::AsyncWait:
+        pad(ind);
+        o += "async_wait();\n";
+        break;
+      case SK::AsyncCopy:
+        pad(ind);
+        o += "async_copy(" + s.outs[0] + ", ";
+        expr(s.val[0]);
+        o += ", " + s.name + ", ";
+        expr(s.idx[0]);
+        o += ");\n";
         break;
       case SK::BarSync:
         pad(ind);

@@ -96,6 +96,12 @@ enum class SK : uint8_t {
   VStore,  // MK+: vstore(arr, i, e0..en-1): arr[i*n + k] = e_k
   Fence,   // MK+: fence(): device-scope memory fence (a no-op for the sequential interpreter)
   WarpSync,  // MK+: warp_sync(): __syncwarp() (a no-op for the lock-step interpreter)
+  // MK+: async_copy(sarr, j, garr, i): the 4 elements garr[4i..4i+3] -> shared sarr[4j..4j+3]
+  // as one 16-byte asynchronous copy (sm_100a cp.async: no register holds the data in flight).
+  // name = garr, idx[0] = i, outs[0] = sarr, val[0] = j. The issuing thread may read the copied
+  // elements only after its next async_wait(); the interpreter lowering copies immediately.
+  AsyncCopy,
+  AsyncWait,  // MK+: async_wait(): this thread's async copies have landed (cp.async.wait_all)
 };
 
 struct Stmt {

@@ -56,6 +56,12 @@ struct Scoped {
         expr(s.idx[0]);
         for (auto& d : s.outs) d = resolve(d);
         break;
+      case SK::AsyncCopy:
+        s.name = resolve(s.name);
+        s.outs[0] = resolve(s.outs[0]);
+        expr(s.idx[0]);
+        expr(s.val[0]);
+        break;
       case SK::If:
         expr(s.val[0]);
         block(s.body);
@@ -267,6 +273,7 @@ class Inliner {
       case SK::Atomic:
       case SK::VLoad:
       case SK::VStore:
+      case SK::AsyncCopy:
         for (auto& e : c.idx) extract(e, out);
         for (auto& e : c.val) extract(e, out);
         out.push_back(std::move(c));
@@ -484,6 +491,13 @@ class Lifter {
           s.name = resolve(s.name);
           expr(s.idx[0]);
           for (auto& d : s.outs) d = resolve(d);
+          out.push_back(std::move(s));
+          break;
+        case SK::AsyncCopy:
+          s.name = resolve(s.name);
+          s.outs[0] = resolve(s.outs[0]);
+          expr(s.idx[0]);
+          expr(s.val[0]);
           out.push_back(std::move(s));
           break;
         case SK::If:
@@ -750,6 +764,22 @@ struct Lowerer {
     if (c.k == SK::Fence) return;     // the interpreter is sequentially consistent
     if (c.k == SK::Atomic) c.bid = 0;  // atomic_add_release -> atomic_add (same reason)
     if (c.k == SK::WarpSync) return;  // ... and runs each warp in lock step
+    if (c.k == SK::AsyncWait) return;  // the lowered copy below has already landed
+    if (c.k == SK::AsyncCopy) {
+      // sarr[4j + k] = garr[4i + k], k = 0..3, both indices evaluated once, copied immediately
+      int id = counter++;
+      std::string gb = "__ag" + std::to_string(id), sb = "__as" + std::to_string(id);
+      Stmt g = decl_init(Ty::Int, gb, binary(Bin::Mul, c.idx[0], lit(4)));
+      g.pos = c.pos;
+      out.push_back(g);
+      out.push_back(decl_init(Ty::Int, sb, binary(Bin::Mul, c.val[0], lit(4))));
+      for (int k = 0; k < 4; ++k) {
+        Expr gi = k == 0 ? var(gb) : binary(Bin::Add, var(gb), lit(k));
+        Expr si = k == 0 ? var(sb) : binary(Bin::Add, var(sb), lit(k));
+        out.push_back(assign_at(c.outs[0], si, index(c.name, gi)));
+      }
+      return;
+    }
     if (c.k == SK::VLoad || c.k == SK::VStore) {
       int id = counter++;
       int n = int(c.k == SK::VLoad ? c.outs.size() : c.val.size());

@@ -54,7 +54,11 @@ RC = [0x0000000000000001, 0x0000000000008082, 0x800000000000808A, 0x800000008000
       0x0000000080008009, 0x000000008000000A, 0x000000008000808B, 0x800000000000008B, 0x8000000000008089,
       0x8000000000008003, 0x8000000000008002, 0x8000000000000080, 0x000000000000800A, 0x800000008000000A,
       0x8000000080008081, 0x8000000000008080, 0x0000000080000001, 0x8000000080008008]
-HPP = 8  # Ethash: nonces of an 8-lane group whose DAG walks are in flight together per lane
+HPP = int(os.environ.get("HF_ETHASH_HPP", "8"))  # Ethash: nonces of an 8-lane group whose DAG walks are in flight together per lane
+# Ethash DAG reads: "ldg" = 128-bit register loads (vload); "async" = 16-byte cp.async copies into a
+# per-thread shared-memory ring (MK+ async_copy / async_wait), so no register holds a page in flight
+ETHASH_LOAD = os.environ.get("HF_ETHASH_LOAD", "ldg")
+ETHASH_TMAX = 512  # async form: the shared ring is sized for intervals of up to 512 threads
 ROT = [[0, 36, 3, 41, 18], [1, 44, 10, 45, 2], [62, 6, 43, 15, 61], [28, 55, 25, 21, 56], [27, 20, 39, 8, 14]]
 
 
@@ -503,6 +507,8 @@ def gen_ethash():
 // multiple block size works (tunable: the partition search sizes it against its partner).""",
            f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], int {p}_dag[], int {p}_rc[], {hp}, int {p}_npages, "
            f"int {p}_nonce0, int {p}_count, int {p}_target", 256, fixed=False)
+    if ETHASH_LOAD == "async":
+        s(f"shared int {p}_ring[{HPP * ETHASH_TMAX * 4}];")
     A = {(x, y): Lane(f"a{x}{y}l", f"a{x}{y}h") for x in range(5) for y in range(5)}
     names = []
     for x in range(5):
@@ -556,8 +562,15 @@ def gen_ethash():
             s(f"pg{h} = ((it + {k}) ^ z{h}) * 16777619 ^ x{h}_{k};")
             bcast8(s, f"pg{h}", "owner")
             s(f"pg{h} = (pg{h} & ({p}_npages - 1)) * 8 + lj;")
+        if ETHASH_LOAD == "async":
+            for h in range(HPP):
+                s(f"async_copy({p}_ring, {h * ETHASH_TMAX} + tid, {p}_dag, pg{h});")
+            s("async_wait();")
         for h in range(HPP):
-            s(f"vload({p}_dag, pg{h}, q0, q1, q2, q3);")
+            if ETHASH_LOAD == "async":
+                s(f"vload({p}_ring, {h * ETHASH_TMAX} + tid, q0, q1, q2, q3);")
+            else:
+                s(f"vload({p}_dag, pg{h}, q0, q1, q2, q3);")
             for j in range(4):
                 s(f"x{h}_{j} = x{h}_{j} * 16777619 ^ q{j};")
     s.ind -= 1

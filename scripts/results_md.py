@@ -1,65 +1,56 @@
-"""Render DESIGN.md §10 tables from a bench JSON line (profiles/r01_bench_full.json)."""
+"""Render DESIGN.md §10 tables from a bench line + its detail file:
+python scripts/results_md.py profiles/r02_bench_line.json profiles/r02_bench_detail.json"""
 import json
+import os
 import sys
 
-d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
-o = []
-ceil = all("ceiling_frac" in p for p in d["pairs"])
-o.append("| pair | grid | d1/d2 | fused µs | seq µs | 2-stream µs | speedup | roofline |" + (" mix ceiling µs (frac) |" if ceil else "")
-         + " naive goto fusion µs | VFuse µs |")
-o.append("|---|---|---|---|---|---|---|---|---|---|" + ("---|" if ceil else ""))
-for p in d["pairs"]:
-    sp = p["speedup"]
-    o.append(f"| {p['pair']} | {p['grid']} | {p['d1']}/{p['d2']}{' cap ' + str(p['reg_cap']) if p['reg_cap'] else ''} | "
-             f"{p['fused_us']:.1f} | {p['seq_us']:.1f} | {p['two_stream_us']:.1f} | "
-             f"{'**%.3f**' % sp if sp > 1.0 else '%.3f' % sp} | {p['roofline_frac']:.3f} | "
-             + (f"{p['ceiling_us']:.1f} ({p['ceiling_frac']:.3f}) | " if ceil else "")
-             + f"{p['naive_fused_us']:.1f} | {p['vertical_us']:.1f} |")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+line = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+d = json.load(open(sys.argv[2]))
+hbm = line["roofline"]["peak"]
+ops = json.load(open(os.path.join(ROOT, "profiles", "crypto_ops.json")))
+o = ["| pair | grid | d1/d2 | fused µs (±95 %) | seq µs | 2-stream µs | speed-up | copy roofline | mix ceiling µs (frac) |",
+     "|---|---|---|---|---|---|---|---|---|"]
+for r in d["results"]:
+    sp = r["speedup"]
+    cap = f" cap {r['reg_cap']}" if r["reg_cap"] else ""
+    o.append(f"| {r['pair']} | {r['grid']} | {r['d1']}/{r['d2']}{cap} | {r['fused_us']:.1f} (±{r['fused_ci95']:.2f}) | "
+             f"{r['seq_us']:.1f} | {r['two_stream_us']:.1f} | {'**%.3f**' % sp if sp > 1 else '%.3f' % sp} "
+             f"(±{r['speedup_ci95']:.3f}) | {r['bytes'] / (hbm * 1e3) / r['fused_us']:.3f} | "
+             + (f"{r['ceiling_us']:.1f} ({r['ceiling_frac']:.3f}) |" if "ceiling_us" in r else "— |"))
+st = d["steps"]
 o.append("")
-o.append(f"Geomean speedup vs min(seq, two-stream): {d['speedup_geomean']:.3f}. Step of all ten (`value`): "
-         f"{d['value']:.1f} µs fused (programmatic dependent launches) vs "
-         + (f"{min(d['unfused_two_stream_step_us'], d.get('unfused_overlap_step_us', 1e30)):.1f} µs for the faster unfused step "
-            f"(step speed-up {d['step_speedup']:.3f}); without overlap the fused step takes "
-            f"{d.get('fused_serial_step_us', float('nan')):.1f} µs. " if 'unfused_overlap_step_us' in d else
-            f"{d['unfused_two_stream_step_us']:.1f} µs unfused on two streams. ") +
-         f"e2e (host buffers, pipelined): {d['e2e']['value'] / 1000:.1f} ms per step "
-         f"({d['e2e']['h2d_bytes_per_step'] / 1e9:.2f} GB up, {d['e2e']['d2h_bytes_per_step'] / 1e9:.2f} GB down); "
-         + (f"reference CPU interpreter: {d['cpu_baseline']['value'] / 1e6:.1f} s per step "
-            f"({d['cpu_baseline']['cores']} processes). " if d.get("cpu_baseline") else "") +
-         f"Clocks {d['clocks']['sm_mhz']:.0f}/{d['clocks']['sm_max_mhz']:.0f} MHz, reasons {d['clocks']['reasons']}.")
-if d.get("ratios"):
-    rr = d["ratios"]
-    rs = sorted({x["target_ratio"] for x in rr["rows"]})
+o.append(f"Geomean speed-up vs min(seq, two-stream): {line['speedup_geomean']:.3f}. Step (`value`): "
+         f"{st['fused_pdl_us']:.1f} µs (ten fused kernels as programmatic dependent launches); without overlap "
+         f"{st['fused_serial_us']:.1f} µs; unfused {st['unfused_two_stream_us']:.1f} µs (two streams per pair) / "
+         f"{st['unfused_pdl_us']:.1f} µs (twenty PDL launches) → step speed-up {line['step_speedup']:.3f}. "
+         f"Sum of the ten mix ceilings: {sum(r.get('ceiling_us', 0) for r in d['results']):.1f} µs. "
+         f"e2e {line['e2e']['value'] / 1000:.1f} ms per step ({line['e2e']['h2d_bytes_per_step'] / 1e9:.2f} GB up, "
+         f"{line['e2e']['d2h_bytes_per_step'] / 1e9:.2f} GB down). Clocks {line['clocks']['sm_mhz']:.0f}/"
+         f"{line['clocks']['sm_max_mhz']:.0f} MHz, reasons {line['clocks']['reasons']}.")
+o.append("")
+o.append("| crypto pair | partition | registers | fused µs | seq µs | 2-stream µs | speed-up | issue bound µs | HBM bound µs | roofline frac |")
+o.append("|---|---|---|---|---|---|---|---|---|---|")
+slots = 148 * 4 * line["clocks"]["sm_mhz"] * 1e6
+for c in d["crypto"]["pairs"]:
+    if c["pair"] == "upsample+blake256":
+        continue
+    a, b = c["pair"].split("+")
+    n = c["nonces"]
+    ti = sum(n[k] * ops[k]["ops_per_nonce"] / 32 for k in (a, b)) / slots * 1e6
+    th = n.get("ethash", 0) * 8192 / (hbm * 1e3)
+    regs = f"budgets {c['interval_regs'][0]}/{c['interval_regs'][1]}" if c.get("interval_regs") else \
+        (f"cap {c['reg_cap']}" if c.get("reg_cap") else f"uncapped ({c['regs']})")
+    sp = c["speedup"]
+    o.append(f"| {c['pair']} | {c['d1']}/{c['d2']} @ {c['grid']} | {regs} | {c['fused_us']:.0f} | {c['seq_us']:.0f} | "
+             f"{c['two_stream_us']:.0f} | {'**%.3f**' % sp if sp > 1 else '%.3f' % sp} | {ti:.0f} | {th:.0f} | "
+             f"{max(ti, th) / c['fused_us']:.3f} |")
+c4 = next((c for c in d["crypto"]["pairs"] if c["pair"] == "upsample+blake256"), None)
+if c4:
     o.append("")
-    o.append("Cells: measured t_b/t_a; fused µs / min(seq, two-stream) µs; speedup.")
-    o.append("")
-    o.append("| pair | " + " | ".join(f"t_b/t_a ≈ {r:g}" for r in rs) + " |")
-    o.append("|---|" + "---|" * len(rs))
-    for pair in dict.fromkeys(x["pair"] for x in rr["rows"]):
-        cells = []
-        for r in rs:
-            x = next(x for x in rr["rows"] if x["pair"] == pair and x["target_ratio"] == r)
-            sp = x["speedup"]
-            cells.append(f"{x['ratio']:.2f}, {x['fused_us']:.1f} / {min(x['seq_us'], x['two_stream_us']):.1f}, "
-                         + ("**%.3f**" % sp if sp > 1.0 else "%.3f" % sp))
-        o.append(f"| {pair} | " + " | ".join(cells) + " |")
-    o.append("")
-    o.append("Geomean speedup per ratio: " + ", ".join(f"{k}: {v:.3f}" for k, v in rr["speedup_geomean"].items()) + ".")
-if d.get("crypto"):
-    o.append("")
-    o.append("| crypto pair | partition | registers | fused µs | seq µs | 2-stream µs | speedup | roofline (bound) |")
-    o.append("|---|---|---|---|---|---|---|---|")
-    for p in d["crypto"]["c3"]:
-        regs = ("budgets %d/%d" % tuple(p["interval_regs"])) if p.get("interval_regs") else (
-            "cap %s" % p["reg_cap"] if p["reg_cap"] else "uncapped (%d)" % p["regs"])
-        r = p.get("roofline") or {}
-        o.append(f"| {p['pair']} | {p['d1']}/{p['d2']} | {regs} | {p['fused_us']:.0f} | {p['seq_us']:.0f} | "
-                 f"{p['two_stream_us']:.0f} | {'**%.3f**' % p['speedup'] if p['speedup'] > 1.0 else '%.3f' % p['speedup']} | {r.get('frac', 0):.2f} issue, {r.get('alu_frac', 0):.2f} ALU pipe |")
-    c4 = d["crypto"]["c4"]
-    b = c4["best"]
-    o.append("")
-    grids = (f" (grids: fused {b['grid']}, members alone {c4['grid_a']}/{c4['grid_b']}, two-stream "
-             f"{c4['two_stream_grids'][0]}/{c4['two_stream_grids'][1]})" if "grid" in b else "")
-    o.append(f"C4 Upsample + BLAKE-256: best d0 {b['d0']} (Upsample {b['d1']}), reg_cap {b['reg_cap']}: {b['us']:.1f} µs vs "
-             f"{c4['seq_us']:.1f} sequential / {c4['two_stream_us']:.1f} two-stream{grids} — **{c4['speedup']:.3f}×**.")
+    o.append(f"C4 Upsample + BLAKE-256: best d0 {c4['d0']} (Upsample {c4['d1']}), "
+             + (f"budgets {c4['interval_regs']}" if c4.get("interval_regs") else f"reg_cap {c4['reg_cap']}")
+             + f", grid {c4['grid']}: {c4['fused_us']:.1f} µs vs {c4['seq_us']:.1f} sequential / "
+               f"{c4['two_stream_us']:.1f} two-stream — **{c4['speedup']:.3f}×** (winner of {len(c4['sweep'])} "
+               f"sweep points re-timed with its baselines' protocol).")
 print("\n".join(o))
