@@ -635,7 +635,8 @@ def main():
         try:
             # ncu dram__bytes_read.sum + dram__bytes_write.sum of this fused kernel, one launch
             t = json.load(open(tpath)).get(f"{da}+{db}")
-            traffic = t["dram_bytes"] if t and t.get("config") == cfgs[dom_i] else None
+            traffic = (t["dram_bytes"] if t and t.get("config") == cfgs[dom_i]
+                       and t.get("algorithmic_bytes") == dom_bytes else None)
         except Exception:
             traffic = None
 

@@ -28,6 +28,9 @@ o.append(f"Geomean speed-up vs min(seq, two-stream): {line['speedup_geomean']:.3
          f"e2e {line['e2e']['value'] / 1000:.1f} ms per step ({line['e2e']['h2d_bytes_per_step'] / 1e9:.2f} GB up, "
          f"{line['e2e']['d2h_bytes_per_step'] / 1e9:.2f} GB down). Clocks {line['clocks']['sm_mhz']:.0f}/"
          f"{line['clocks']['sm_max_mhz']:.0f} MHz, reasons {line['clocks']['reasons']}.")
+if not d.get("crypto"):
+    print("\n".join(o))
+    sys.exit(0)
 o.append("")
 o.append("| crypto pair | partition | registers | fused µs | seq µs | 2-stream µs | speed-up | issue bound µs | HBM bound µs | roofline frac |")
 o.append("|---|---|---|---|---|---|---|---|---|---|")
