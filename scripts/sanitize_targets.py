@@ -3,7 +3,8 @@ synccheck): named-barrier rewriting must not introduce shared-memory races or ba
   compute-sanitizer --tool racecheck python scripts/sanitize_targets.py
 Covers: corpus pairs (reference Mini-Kernel), the ten DL pairs (B200 forms, parity sizes, two
 splits), the crypto pairs (one register cap and per-interval budgets), the hand-off BatchNorm,
-and a CUDA-frontend pair."""
+a CUDA-frontend pair, and (round 2) dynamic interval scheduling (block- and warp-level queues,
+two launches each) and an MK+ async_copy kernel."""
 import os
 import sys
 
@@ -47,6 +48,19 @@ m = hf.Module.fused(open(os.path.join(cu, "histogram.cu")).read(), open(os.path.
                     128, 896)
 img = hf.Image(corpus["images"]["histogram"]).merge(hf.Image(corpus["images"]["batchnorm"])).upload()
 m.run(img)
+n += 1
+for a, b, vg in [("bn", "hist", (8, 37)), ("im2col", "upsample", (7, 3)), ("hist", "maxpool", (13, 4))]:
+    wa, wb = P.MEMBERS[a].sizes["parity"](), P.MEMBERS[b].sizes["parity"]()
+    img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
+    m = hf.Module.fused_opts(P.source("b200", P.MEMBERS[a].stem), P.source("b200", P.MEMBERS[b].stem), 256, 256,
+                             vgrid=vg, grid=5, specialize=img)
+    for _ in range(2):
+        m.run(img, 5)
+        n += 1
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import test_async_copy as TA  # noqa: E402
+img = hf.Image(TA.IMG).upload()
+hf.Module.kernel(TA.SRC).run(img)
 n += 1
 import ctypes  # noqa: E402
 assert ctypes.CDLL("libcudart.so.12").cudaDeviceSynchronize() == 0
