@@ -624,7 +624,11 @@ def main():
 
     crypto_res = None
     if not args.no_crypto:
-        crypto_res = crypto_suite(hf, torch, args, D, stream, sm_mhz=clk.get("sm_mhz"), hbm_peak=hbm_peak)
+        try:  # C3/C4 are reported beside the C2 step; a failure there must not cost the step's line
+            crypto_res = crypto_suite(hf, torch, args, D, stream, sm_mhz=clk.get("sm_mhz"), hbm_peak=hbm_peak)
+        except hf.HFuseError as e:
+            print(f"crypto suite failed: {e}", file=sys.stderr)
+            crypto_res = None
     ratio_res = None
     if world == 1 and args.ratios != "none":
         ratio_res = ratio_study(hf, P, pair_list, src, shape, grids, d0s, stream, args)
