@@ -331,6 +331,13 @@ def best_two_stream(hf, ka, kb, img, ga, gb, grids, stream, reps, samples):
     return best
 
 
+def fused_grids(d0, waves):
+    """Launch grids tried for a fused block of d0 threads: whole multiples (1, 2, 4, ... waves) of
+    the CTAs that fit the B200 at once (148 SMs x 2048 threads / d0 per SM)."""
+    resident = 148 * (2048 // d0)
+    return [resident * w for w in waves]
+
+
 def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3):
     """Device split search over block size d0 x launch grid (search_config per grid, steady
     graph protocol), then the `top` fastest distinct points re-timed with a longer graph (the
@@ -338,7 +345,7 @@ def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3):
     Returns (config dict, compact trace)."""
     trace = []
     for d0 in d0s:
-        for g in grids if d0 == 1024 else [2 * x for x in grids]:
+        for g in fused_grids(d0, args.waves):
             rg = hf.search(sa, sb, img, d0=d0, grid=g, reps=args.search_reps, warmup=1, specialize=True,
                            flush_l2=False, granularity=args.granularity)
             trace += [(d0, g, t["d1"], t["reg_cap"], round(t["us"], 2)) for t in rg["trace"]]
@@ -393,7 +400,9 @@ def main():
     ap.add_argument("--search-reps", type=int, default=5)
     ap.add_argument("--reps", type=int, default=20, help="repetitions per timing graph")
     ap.add_argument("--samples", type=int, default=7, help="graph samples per timed variant")
-    ap.add_argument("--d0s", default="1024,512", help="fused block sizes searched for the DL pairs")
+    ap.add_argument("--d0s", default="1024,768,640,512", help="fused block sizes searched for the DL pairs")
+    ap.add_argument("--waves", default="1,2,4,8,16",
+                    help="fused launch grids searched, in waves of the CTAs resident at once")
     ap.add_argument("--shapes", default="conv2", choices=["conv2", "conv3"],
                     help="DL tensor shapes: ResNet-50 conv2_x (the C2 configuration, default) or conv3_x")
     ap.add_argument("--granularity", type=int, default=64,
@@ -421,6 +430,7 @@ def main():
     keys = sorted({k for p in pair_list for k in p})
     grids = [int(g) for g in args.grids.split(",")]
     d0s = [int(x) for x in args.d0s.split(",")]
+    args.waves = [int(x) for x in args.waves.split(",")]
     stream = torch.cuda.current_stream()
     shape = "full" if args.shapes == "conv2" else args.shapes
     R, S = args.reps, args.samples

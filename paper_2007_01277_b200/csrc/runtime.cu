@@ -628,7 +628,8 @@ GraphTiming time_graph(Mode mode, const Module& a, const Module* b, Image& img, 
   HF_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
   HF_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
   HF_CUDA(cudaEventCreateWithFlags(&order, cudaEventDisableTiming));
-  std::vector<cudaEvent_t> ev(size_t(samples) + 1);
+  std::vector<cudaEvent_t> ev(2);
+  std::vector<double> us;
   for (auto& e : ev) HF_CUDA(cudaEventCreate(&e));
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -646,6 +647,9 @@ GraphTiming time_graph(Mode mode, const Module& a, const Module* b, Image& img, 
     HF_CUDA(cudaEventRecord(order, user));
     HF_CUDA(cudaStreamWaitEvent(cs, order, 0));
     HF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    // timing events inside the graph (external event-record nodes): a sample is the graph's own
+    // execution, without the gap between consecutive graph launches
+    HF_CUDA(cudaEventRecordWithFlags(ev[0], cs, cudaEventRecordExternal));
     for (int r = 0; r < reps; ++r) {
       if (mode == Mode::Single) {
         launch_raw(a, ga, ba.args.data(), cs);
@@ -661,26 +665,23 @@ GraphTiming time_graph(Mode mode, const Module& a, const Module* b, Image& img, 
         HF_CUDA(cudaStreamWaitEvent(cs, join, 0));
       }
     }
+    HF_CUDA(cudaEventRecordWithFlags(ev[1], cs, cudaEventRecordExternal));
     HF_CUDA(cudaStreamEndCapture(cs, &graph));
     HF_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     HF_CUDA(cudaGraphLaunch(exec, cs));  // warm-up: one full graph
-    HF_CUDA(cudaEventRecord(ev[0], cs));
+    HF_CUDA(cudaStreamSynchronize(cs));
     for (int i = 0; i < samples; ++i) {
       HF_CUDA(cudaGraphLaunch(exec, cs));
-      HF_CUDA(cudaEventRecord(ev[size_t(i) + 1], cs));
+      HF_CUDA(cudaEventSynchronize(ev[1]));
+      float ms = 0;
+      HF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      us.push_back(double(ms) * 1000.0 / reps);
     }
-    HF_CUDA(cudaEventSynchronize(ev[size_t(samples)]));
   } catch (...) {
     cudaStreamEndCapture(cs, &graph);  // no-op unless still capturing
     cudaStreamSynchronize(cs);
     cleanup();
     throw;
-  }
-  std::vector<double> us;
-  for (int i = 0; i < samples; ++i) {
-    float ms = 0;
-    HF_CUDA(cudaEventElapsedTime(&ms, ev[size_t(i)], ev[size_t(i) + 1]));
-    us.push_back(double(ms) * 1000.0 / reps);
   }
   HF_CUDA(cudaEventRecord(order, cs));
   HF_CUDA(cudaStreamWaitEvent(user, order, 0));

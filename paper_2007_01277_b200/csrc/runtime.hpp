@@ -87,11 +87,12 @@ Timing time(Mode mode, const Module& a, const Module* b, Image& img, int grid_a,
             int reps, bool flush_l2, void* stream = nullptr);
 
 // Graph protocol: `reps` back-to-back repetitions of the variant (a; a then b; a || b on two
-// streams) captured as ONE CUDA graph, launched `samples` times between consecutive events on
-// one stream, no host synchronization inside the timed region. Each sample yields the mean
-// time per repetition (no per-repetition front-end or event cost, and the two-stream fork/join
-// is a graph edge rather than an event wait); the summary is over samples with a Student-t
-// 95 % half-width. Every repetition's working set must exceed L2 for steady-state HBM numbers
+// streams) captured as ONE CUDA graph between two timing-event nodes (external event records
+// inside the graph), launched `samples` times; no host synchronization inside the timed region.
+// Each sample yields the mean time per repetition of the graph's own execution (no
+// per-repetition front-end or event cost, no gap between graph launches, and the two-stream
+// fork/join is a graph edge rather than an event wait); the summary is over samples with a
+// Student-t 95 % half-width. Every repetition's working set must exceed L2 for steady-state HBM numbers
 // (the caller's choice; nothing is flushed).
 struct GraphTiming {
   double mean_us = 0, median_us = 0, min_us = 0, max_us = 0, ci95_us = 0;
