@@ -623,9 +623,12 @@ def main():
             step()  # one clean step + the collective
             torch.cuda.synchronize()
             parity["merged_bn"] = check_merged_bn(P, shape, merged["out"], layout, rank) if rank == 0 else None
-        oks = D.all_max([0.0 if parity["ok"] else 1.0])[0]
+        bad = 0.0 if parity["ok"] else 1.0
+        if parity.get("merged_bn") is not None and not parity["merged_bn"]["ok"]:
+            bad = 1.0
+        oks = D.all_max([bad])[0]  # every rank leaves together when any check failed
         parity["all_ranks_ok"] = oks == 0.0
-        if oks != 0.0 or (parity.get("merged_bn") is not None and not parity["merged_bn"]["ok"]):
+        if oks != 0.0:
             if rank == 0:
                 print(json.dumps({"error": "parity check failed", "parity": parity})[:4000], file=sys.stderr)
             D.close()
