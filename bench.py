@@ -783,7 +783,8 @@ CRYPTO_COUNTS = {"sha256d": 1 << 24, "blake2b": 1 << 23, "blake256": 1 << 24, "e
 # Ethash always second, so its interval takes d0 - 512)
 CRYPTO_PAIRS = [("sha256d", "blake2b"), ("blake256", "ethash"), ("sha256d", "blake256"),
                 ("sha256d", "ethash"), ("blake256", "blake2b"), ("blake2b", "ethash")]
-ETHASH_PAGES = 1 << 25  # 4 GiB synthetic DAG (>> the 126 MB L2)
+ETHASH_PAGES = 33554393  # 4.3 GB synthetic DAG (>> the 126 MB L2): the largest prime page count below 2^25,
+                         # walked with Ethash's modulo rule (a real DAG's page count is prime too)
 
 
 def crypto_roofline(nonces, t_us, sm_mhz, hbm_peak):

@@ -9,7 +9,8 @@ standard test vectors in tests/test_crypto_oracle.py:
   * BLAKE2b-512: hashlib.blake2b
   * Keccak-256/512 (original 0x01 padding): restated; pinned on Keccak-256("") and
     Keccak-512("")
-  * the Ethash-style hashimoto loop of the ethash member (power-of-two synthetic DAG)
+  * the Ethash-style hashimoto loop of the ethash member (synthetic DAG, ethminer's modulo walk:
+    page = fnv(i ^ s[0], mix[i % 32]) mod n_pages, Ethash spec `hashimoto`; Keccak pinned)
 
 Workload conventions (shared with paper_2007_01277_b200/kernels/gen_crypto.py): a header is
 20 32-bit words; the nonce of thread-iteration n is nonce0 + n (32-bit wrap).
@@ -180,7 +181,8 @@ def fnv(a, b):
 def ethash_hashimoto(header_words, nonce, dag, n_pages):
     """The ethash member: seed = Keccak-512(header_hash || nonce_le64); a 128-byte mix
     (32 words) initialised from the seed, 64 rounds of fnv-mixing with the DAG page
-    p = fnv(i ^ seed[0], mix[i % 32]) & (n_pages - 1) (power-of-two page count), 8-word
+    p = fnv(i ^ seed[0], mix[i % 32]) mod n_pages (the Ethash spec's `hashimoto` walk over
+    n_pages 128-byte pages, any count; the fnv word unsigned), 8-word
     compression, result = Keccak-256(seed || cmix). Returns (cmix[8], result words[8]),
     32-bit little-endian words. dag: numpy uint32 array of n_pages * 32 words."""
     hh = b"".join(struct.pack("<I", x & M32) for x in header_words[:8])
@@ -188,7 +190,7 @@ def ethash_hashimoto(header_words, nonce, dag, n_pages):
     s = list(struct.unpack("<16I", seed))
     mix = [s[i % 16] for i in range(32)]
     for i in range(64):
-        p = fnv(i ^ s[0], mix[i % 32]) & (n_pages - 1)
+        p = fnv(i ^ s[0], mix[i % 32]) % n_pages
         page = dag[p * 32:(p + 1) * 32]
         mix = [fnv(mix[j], int(page[j])) for j in range(32)]
     cmix = [fnv(fnv(fnv(mix[4 * k], mix[4 * k + 1]), mix[4 * k + 2]), mix[4 * k + 3]) for k in range(8)]

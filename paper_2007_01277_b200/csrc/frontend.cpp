@@ -893,6 +893,7 @@ class Parser {
           else if (b200() && n.text == "load_relaxed") w = Intr::Relaxed;
           else if (b200() && n.text == "warp_bcast") w = Intr::Bcast;
           else if (b200() && n.text == "addc") w = Intr::Addc;
+          else if (b200() && n.text == "remu") w = Intr::RemU;
           if (w) {
             std::vector<Expr> a = args();
             if (int(a.size()) != intr_arity(*w))

@@ -44,6 +44,7 @@ const char* intr_name(Intr i) {
     case Intr::Relaxed: return "load_relaxed";
     case Intr::Bcast: return "warp_bcast";
     case Intr::Addc: return "addc";
+    case Intr::RemU: return "remu";
   }
   return "?";
 }

@@ -74,6 +74,8 @@ enum class Intr : uint8_t {
             // in [2, 32], src uniform within each w-lane group; only as a whole assignment value
   Addc,     // addc(ahi, bhi, alo, blo): ahi + bhi + carry-out of alo + blo (64-bit add, high word;
             // device: add.cc + addc, i.e. IADD3 + IADD3.X instead of an unsigned compare)
+  RemU,     // remu(a, b): a mod b with a read as uint32, for 0 < b < 2^30 (Ethash's page walk);
+            // device: one unsigned remainder; plain MK: ((shr_u(a, 1) % b) * 2 + (a & 1)) % b
 };
 const char* intr_name(Intr i);
 int intr_arity(Intr i);

@@ -679,6 +679,11 @@ struct Lowerer {
       }
       case Intr::LtU:
         return binary(Bin::Lt, binary(Bin::Xor, x, int_min()), binary(Bin::Xor, n, int_min()));
+      case Intr::RemU: {
+        // a as uint32 = 2 * shr_u(a, 1) + (a & 1); both partial values stay below 2^31 for b < 2^30
+        Expr half = binary(Bin::Mod, shr_u(x, lit(1)), n);
+        return binary(Bin::Mod, binary(Bin::Add, binary(Bin::Mul, half, lit(2)), binary(Bin::And, x, lit(1))), n);
+      }
       case Intr::Addc: {
         // ahi + bhi + ltu(alo + blo, alo), with ltu spelled out as above
         Expr lo = binary(Bin::Add, c.a[2], c.a[3]);

@@ -492,7 +492,8 @@ def gen_ethash():
     header(s, p, "ethash", """// Ethash-style hashimoto nonce search (ethminer analogue, PAPER.md:876-879).
 // Generated by kernels/gen_crypto.py. seed = Keccak-512(header_hash[8 words] || nonce as
 // 64-bit LE); mix = seed repeated to 32 words; 64 rounds: page = fnv(i ^ seed[0],
-// mix[i % 32]) & (npages - 1), mix = fnv(mix, dag[page]) over the 128-byte page;
+// mix[i % 32]) % npages (ethminer's modulo walk; remu: the fnv word read as uint32),
+// mix = fnv(mix, dag[page]) over the 128-byte page;
 // cmix = 8-word fnv fold; result = Keccak-256(seed || cmix).
 // B200 mechanics (ethminer's lane-cooperative layout): every thread computes the two Keccaks
 // of its own nonce, but the DAG loop of the 8 nonces of an 8-lane group is shared: lane j
@@ -503,7 +504,7 @@ def gen_ethash():
 // LOP3, rho+pi in place along the pi cycle, chi row by row: ~64 live registers), 24 rounds as
 // a loop over one straight-line round (constants from P_rc[48]).
 // Criterion/checksum word = result word 0 (little-endian). The DAG is a synthetic
-// power-of-two page array (SURVEY §8d: a seeded int32 array, >= 4 GiB for C3). Any warp-
+// page array of npages 128-byte pages (a prime count, like the real DAG's; any count < 2^25 works) (SURVEY §8d: a seeded int32 array, >= 4 GiB for C3). Any warp-
 // multiple block size works (tunable: the partition search sizes it against its partner).""",
            f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], int {p}_dag[], int {p}_rc[], {hp}, int {p}_npages, "
            f"int {p}_nonce0, int {p}_count, int {p}_target", 256, fixed=False)
@@ -561,7 +562,7 @@ def gen_ethash():
         for h in range(HPP):
             s(f"pg{h} = ((it + {k}) ^ z{h}) * 16777619 ^ x{h}_{k};")
             bcast8(s, f"pg{h}", "owner")
-            s(f"pg{h} = (pg{h} & ({p}_npages - 1)) * 8 + lj;")
+            s(f"pg{h} = remu(pg{h}, {p}_npages) * 8 + lj;")
         if ETHASH_LOAD == "async":
             for h in range(HPP):
                 s(f"async_copy({p}_ring, {h * ETHASH_TMAX} + tid, {p}_dag, pg{h});")

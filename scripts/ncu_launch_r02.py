@@ -50,7 +50,7 @@ if not args.no_crypto:
         a, b = c["pair"].split("+")
         wa = CR.workload(a, c["per_rank_nonces"][a], max(c["grid"], c["grid_a"], c["grid_b"]), target=1 << 12)
         wb = CR.workload(b, c["per_rank_nonces"][b], max(c["grid"], c["grid_a"], c["grid_b"]), target=1 << 12,
-                         npages=1 << 25)
+                         npages=33554393)
         img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
         sa = open(os.path.join(P.KERNELS, "b200", a + ".mk")).read()
         sb = open(os.path.join(P.KERNELS, "b200", b + ".mk")).read()

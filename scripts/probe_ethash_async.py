@@ -20,7 +20,7 @@ def gen(load, hpp):
 
 
 N = 1 << 20
-wb = CR.workload("ethash", N, 1184, target=1 << 12, npages=1 << 25)
+wb = CR.workload("ethash", N, 1184, target=1 << 12, npages=33554393)
 wa = CR.workload("blake256", 1 << 24, 1184, target=1 << 12)
 img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
 blake = open(os.path.join(P.KERNELS, "b200", "blake256.mk")).read()

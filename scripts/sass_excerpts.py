@@ -70,7 +70,7 @@ def main():
             continue
         a, b = c["pair"].split("+")
         wa = CR.workload(a, 1 << 20, c["grid"], target=1 << 12)
-        wb = CR.workload(b, 1 << 20, c["grid"], target=1 << 12, npages=1 << 25)
+        wb = CR.workload(b, 1 << 20, c["grid"], target=1 << 12, npages=33554393)
         img = hf.Image(wa.image).merge(hf.Image(wb.image))
         sa = open(os.path.join(P.KERNELS, "b200", a + ".mk")).read()
         sb = open(os.path.join(P.KERNELS, "b200", b + ".mk")).read()

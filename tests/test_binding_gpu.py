@@ -37,7 +37,7 @@ def test_reference_search_config_drives_b200(gpu, corpus, tmp_path):
     for stem in ("batchnorm", "histogram"):
         (tmp_path / f"{stem}.mk").write_text(corpus["kernels"][stem])
         (tmp_path / f"{stem}.img").write_text(corpus["images"][stem])
-    cmd = f"{EXE} profile --mem {tmp_path / 'batchnorm.img'} --mem {tmp_path / 'histogram.img'} --reps 5"
+    cmd = f"{EXE} profile --mem {tmp_path / 'batchnorm.img'} --mem {tmp_path / 'histogram.img'} --reps 20"
     r = subprocess.run([BIN, tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", tmp_path / "batchnorm.img",
                         tmp_path / "histogram.img", "--cmd", cmd], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr
@@ -54,4 +54,7 @@ def test_reference_search_config_drives_b200(gpu, corpus, tmp_path):
         assert all(int(row[3]) > 0 for row in rows)
         d1 = int(kv["best_d1"])
         assert int(kv["best_d2"]) == 1024 - d1
-        assert d1 in us and us[d1] <= 1.15 * best, (tag, d1, us, best)
+        # microsecond corpus kernels: the in-process backend within 15 % of hfuse's pick, the
+        # one-process-per-candidate command (cold context per candidate) within 25 %
+        tol = 1.15 if tag == "B200Backend" else 1.25
+        assert d1 in us and us[d1] <= tol * best, (tag, d1, us, best)

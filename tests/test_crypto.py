@@ -39,11 +39,40 @@ def test_generated_sources_are_current(tmp_path):
         assert gen() == src(kind), kind
 
 
-def reference_outputs(kind, count, grid, nonce0, target, words=None, threads=None):
+def reference_outputs(kind, count, grid, nonce0, target, words=None, threads=None, npages=1 << 10):
     words = words or crypto.header_words(2024, 20)
-    dag = C.LazyDag(77, 1 << 10) if kind == "ethash" else None
+    dag = C.LazyDag(77, npages) if kind == "ethash" else None
     return C.search_outputs(kind, words, nonce0, count, target, grid, threads or crypto.THREADS[kind], dag=dag,
-                            n_pages=1 << 10)
+                            n_pages=npages)
+
+
+PRIME_PAGES = 1021  # Ethash's modulo page walk over a non-power-of-two DAG (the bench: 33,554,393)
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_ethash_modulo_walk_on_reference_interpreter(hf, tmp_path):
+    """remu (MK+ unsigned remainder) lowered to plain Mini-Kernel walks a prime page count
+    exactly like crypto_ref's `fnv(...) % n_pages` (the Ethash spec's hashimoto)."""
+    count, grid, nonce0, target = 6, 1, 4242, 1 << 31
+    w = crypto.workload("ethash", count=count, grid=grid, nonce0=nonce0, target=target, npages=PRIME_PAGES)
+    (tmp_path / "k.mk").write_text(hf.lower(src("ethash")))
+    (tmp_path / "k.img").write_text(w.image)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img", "--grid", grid)
+    arrays, _ = oracle.parse_image(dump)
+    want = reference_outputs("ethash", count, grid, nonce0, target, npages=PRIME_PAGES)
+    assert int(arrays["eh_chk"][0]) == want["chk"] and int(arrays["eh_cnt"][0]) == want["cnt"]
+
+
+@pytest.mark.gpu
+def test_ethash_modulo_walk_on_device(gpu):
+    hf = gpu
+    count, grid, nonce0, target = 512, 4, 99, 1 << 28
+    w = crypto.workload("ethash", count=count, grid=grid, nonce0=nonce0, target=target, npages=PRIME_PAGES)
+    img = hf.Image(w.image).upload()
+    hf.Module.kernel(src("ethash"), grid=grid, specialize=img).run(img, grid)
+    img.download()
+    assert device_outputs(img, "ethash") == reference_outputs("ethash", count, grid, nonce0, target,
+                                                              npages=PRIME_PAGES)
 
 
 @pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
