@@ -208,6 +208,11 @@ typedef struct hf_fuse_opts {
   int vgrid1, vgrid2;
   int grid;
   int min_blocks;
+  int split_grid; /* heterogeneous CTA partition (0 = off): blocks below it run both members
+                     (member 1 sees a grid of split_grid blocks); blocks above give all d0 threads
+                     to member 2 as d0/d2 sub-blocks (member 2 sees one grid of split_grid +
+                     (grid - split_grid) * d0/d2 blocks of d2 threads). Needs a barrier- and
+                     shared-memory-free 1-D member 2 and d0 % d2 == 0 (HF_E_INVALID_ARGUMENT). */
 } hf_fuse_opts;
 int hf_build_fused_opts(const char* src1, const char* src2, int d1, int d2, const hf_fuse_opts* opts,
                         const hf_image* specialize, hf_module** out, hf_error* err);

@@ -107,6 +107,7 @@ hf::rt::Module build_fused_opts(const char* s1, const char* s2, int d1, int d2, 
   o.regs2 = fo.regs2;
   o.vgrid1 = fo.vgrid1;
   o.vgrid2 = fo.vgrid2;
+  o.split_grid = fo.split_grid;
   o.specialize = scalars_of(spec);
   return hf::rt::compile(hf::emit_sm100(r.fused, o), budgets ? std::nullopt : r.fused.cfg.reg_cap);
 }

@@ -133,6 +133,12 @@ struct Sm100Options {
   // with vgridN blocks (blocks are independent in CUDA); per virtual block the interval's
   // locals and shared arrays start zeroed, as in the interpreter (exec.cpp:291).
   int vgrid1 = 0, vgrid2 = 0;
+  // Heterogeneous CTA partition (fused kernels only; 0 = off): blocks below split_grid run both
+  // members (member 1 sees a grid of split_grid blocks), blocks above give every thread to member
+  // 2 as d0/d2 sub-blocks (member 2 sees one grid of split_grid + (grid - split_grid) * d0/d2
+  // blocks of d2 threads). For a member 1 with a fixed natural grid (BatchNorm's one block per
+  // channel) next to a grid-stride member 2 without barriers or shared memory.
+  int split_grid = 0;
 };
 
 struct Sm100Param {

@@ -80,7 +80,7 @@ class _ModInfo(C.Structure):
 
 class _FuseOpts(C.Structure):
     _fields_ = [("regcap", C.c_int), ("regs1", C.c_int), ("regs2", C.c_int), ("vgrid1", C.c_int),
-                ("vgrid2", C.c_int), ("grid", C.c_int), ("min_blocks", C.c_int)]
+                ("vgrid2", C.c_int), ("grid", C.c_int), ("min_blocks", C.c_int), ("split_grid", C.c_int)]
 
 
 class _Timing(C.Structure):
@@ -430,12 +430,14 @@ class Module:
 
     @classmethod
     def fused_opts(cls, src1: str, src2: str, d1: int, d2: int, regcap="off", regs=None, vgrid=None,
-                   grid: int = 0, min_blocks: int = 0, specialize: Optional["Image"] = None) -> "Module":
+                   grid: int = 0, min_blocks: int = 0, specialize: Optional["Image"] = None,
+                   split_grid: int = 0) -> "Module":
         """Every B200 option (hf_build_fused_opts): regcap, per-interval budgets regs=(r1, r2),
-        dynamic interval scheduling vgrid=(virtual grid of member 1, of member 2)."""
+        dynamic interval scheduling vgrid=(virtual grid of member 1, of member 2), heterogeneous
+        CTA partition split_grid (blocks below it fused, above it member 2 only)."""
         r1, r2 = regs or (0, 0)
         v1, v2 = vgrid or (0, 0)
-        o = _FuseOpts(_regcap(regcap), r1, r2, v1, v2, grid, min_blocks)
+        o = _FuseOpts(_regcap(regcap), r1, r2, v1, v2, grid, min_blocks, split_grid)
         h, err = C.c_void_p(), _Err()
         _check(_lib.hf_build_fused_opts(src1.encode(), src2.encode(), d1, d2, C.byref(o),
                                         specialize._h if specialize else None, C.byref(h), C.byref(err)), err)
