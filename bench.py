@@ -338,7 +338,7 @@ def fused_grids(d0, waves):
     return [resident * w for w in waves]
 
 
-def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3):
+def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3, natural=0):
     """Device split search over block size d0 x launch grid (search_config per grid, steady
     graph protocol), then the `top` fastest distinct points re-timed with a longer graph (the
     minimum of a few hundred short samples is biased low; the re-timing picks on equal terms).
@@ -349,24 +349,73 @@ def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3):
             rg = hf.search(sa, sb, img, d0=d0, grid=g, reps=args.search_reps, warmup=1, specialize=True,
                            flush_l2=False, granularity=args.granularity)
             trace += [(d0, g, t["d1"], t["reg_cap"], round(t["us"], 2)) for t in rg["trace"]]
+    cands = [({"d1": d1, "d2": d0 - d1, "reg_cap": None if cap in ("none", None) else int(cap),
+               "interval_regs": None, "split_grid": 0, "grid": g}, us) for d0, g, d1, cap, us in trace]
+    if args.split and split_member(sb):
+        cands += split_candidates(hf, sa, sb, img, stream, args, natural)
     best = None
-    for d0, g, d1, cap, _ in sorted(trace, key=lambda t: t[4])[:top]:
-        cfg = {"d1": d1, "d2": d0 - d1, "reg_cap": None if cap in ("none", None) else int(cap),
-               "interval_regs": None, "grid": g}
+    for cfg, _ in sorted(cands, key=lambda c: c[1])[:top]:
         m = build_fused(hf, sa, sb, cfg, img)
-        t = gtime(hf, "single", m, None, img, g, 0, stream, 10, 5)["mean_us"]
+        t = gtime(hf, "single", m, None, img, cfg["grid"], 0, stream, 10, 5)["mean_us"]
         if best is None or t < best[1]:
             best = (cfg, t)
         del m
+    trace += [("split", c["grid"], c["d1"], c["d2"], c["split_grid"], c["reg_cap"], round(us, 2))
+              for c, us in cands if c["split_grid"]]
     return best[0], trace
 
 
+def natural_grid(key, w):
+    """A member's own block count when its blocks are fixed units of work (BatchNorm: one block
+    per channel), else 0 (grid-stride members take any grid)."""
+    if key == "bn":
+        return int(w.image.split("scalar bn_C int32 ")[1].split()[0])
+    return 0
+
+
+def split_member(src):
+    """Whether a member can fill whole CTAs as sub-blocks (heterogeneous partition): no barriers,
+    shared memory or fences."""
+    code = "\n".join(line.split("//")[0] for line in src.splitlines())
+    return not any(tok in code for tok in ("syncthreads", "bar_sync", "shared ", "fence("))
+
+
+def split_candidates(hf, sa, sb, img, stream, args, natural=0):
+    """Heterogeneous CTA partitions (split_grid): blocks below B1 run both members, blocks above
+    give all d0 threads to member 2 as d0/d2 sub-blocks. B1 = the first member's natural grid
+    when it has one (BatchNorm: one block per channel), else a few multiples of the SM count.
+    Modules are NVRTC-compiled on a thread pool, then timed like the static points."""
+    from concurrent.futures import ThreadPoolExecutor
+    b1s = [natural] if natural else [296, 592, 1184]
+    shapes = [(d0, d0 // k) for d0 in (1024, 768, 512) for k in (2, 4, 8) if d0 // k >= 64 and (d0 // k) % 32 == 0]
+    specs = [(d0 - d2, d2, cap, b1) for d0, d2 in shapes for cap in (None, 32) for b1 in b1s]
+
+    def build(spec):
+        d1, d2, cap, b1 = spec
+        try:
+            return spec, hf.Module.fused_opts(sa, sb, d1, d2, regcap=cap or "off", split_grid=b1, grid=b1,
+                                              specialize=img)
+        except hf.HFuseError:
+            return spec, None
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        mods = list(pool.map(build, specs))
+    out = []
+    for (d1, d2, cap, b1), m in mods:
+        if m is None:
+            continue
+        d0 = d1 + d2
+        res = 148 * (2048 // d0)
+        for g in sorted({max(b1, res), b1 + res, 2 * b1 + res, 4 * res, 8 * res, 16 * res}):
+            if g < b1:
+                continue
+            t = gtime(hf, "single", m, None, img, g, 0, stream, args.search_reps, 3)["mean_us"]
+            out.append(({"d1": d1, "d2": d2, "reg_cap": cap, "interval_regs": None, "split_grid": b1, "grid": g}, t))
+        del m
+    return out
+
+
 def build_fused(hf, sa, sb, cfg, img):
-    if cfg.get("interval_regs"):
-        return hf.Module.fused_regs(sa, sb, cfg["d1"], cfg["d2"], *cfg["interval_regs"], grid=cfg["grid"],
-                                    specialize=img)
-    return hf.Module.fused(sa, sb, cfg["d1"], cfg["d2"], regcap=cfg["reg_cap"] or "off", grid=cfg["grid"],
-                           specialize=img)
+    return hf.Module.from_config(sa, sb, cfg, specialize=img)
 
 
 def ceiling(hf, P, read_b, write_b, grids, stream, reps, samples):
@@ -398,6 +447,8 @@ def main():
     ap.add_argument("--grids", default="296,592,1184,2368",
                     help="launch grids tried for every DL member and fused pair (multiples of 148 SMs)")
     ap.add_argument("--search-reps", type=int, default=5)
+    ap.add_argument("--no-split", dest="split", action="store_false",
+                    help="skip the heterogeneous CTA partitions (split_grid) in the configuration search")
     ap.add_argument("--reps", type=int, default=20, help="repetitions per timing graph")
     ap.add_argument("--samples", type=int, default=7, help="graph samples per timed variant")
     ap.add_argument("--d0s", default="1024,768,640,512", help="fused block sizes searched for the DL pairs")
@@ -456,7 +507,8 @@ def main():
             mgrid[k] = min(ts, key=ts.get)
         cfgs, traces = [], {}
         for i, (a, b) in enumerate(pair_list):
-            cfg, trace = search_pair(hf, src[a], src[b], imgs[i], d0s, grids, stream, args)
+            cfg, trace = search_pair(hf, src[a], src[b], imgs[i], d0s, grids, stream, args,
+                                     natural=natural_grid(a, work[a]))
             cfgs.append(cfg)
             traces[f"{a}+{b}"] = trace
         plan = {"mgrid": mgrid, "cfgs": cfgs, "traces": traces}
@@ -986,7 +1038,8 @@ def ratio_study(hf, P, pair_list, src, shape, grids, d0s, stream, args):
                 ts = {g: gtime(hf, "single", k, None, img, g, 0, stream, 5, 3)["mean_us"] for g in grids}
                 g = min(ts, key=ts.get)
                 alone[name] = (g, ts[g])
-            cfg, _ = search_pair(hf, src[a], src[b], img, d0s, grids, stream, args)
+            cfg, _ = search_pair(hf, src[a], src[b], img, d0s, grids, stream, args,
+                                 natural=natural_grid(a, wa))
             grid = cfg["grid"]
             m = build_fused(hf, src[a], src[b], cfg, img)
             tf = gtime(hf, "single", m, None, img, grid, 0, stream, args.reps, 5)["mean_us"]

@@ -444,6 +444,20 @@ class Module:
         return cls(h)
 
     @classmethod
+    def from_config(cls, src1: str, src2: str, cfg: dict, specialize: Optional["Image"] = None) -> "Module":
+        """The fused module of a search / bench configuration dict: d1, d2, grid and one of
+        reg_cap (None = uncapped), interval_regs (per-interval budgets) or split_grid
+        (heterogeneous CTA partition, with reg_cap)."""
+        if cfg.get("interval_regs"):
+            return cls.fused_regs(src1, src2, cfg["d1"], cfg["d2"], *cfg["interval_regs"], grid=cfg["grid"],
+                                  specialize=specialize)
+        if cfg.get("split_grid"):
+            return cls.fused_opts(src1, src2, cfg["d1"], cfg["d2"], regcap=cfg.get("reg_cap") or "off",
+                                  grid=cfg["grid"], split_grid=cfg["split_grid"], specialize=specialize)
+        return cls.fused(src1, src2, cfg["d1"], cfg["d2"], regcap=cfg.get("reg_cap") or "off", grid=cfg["grid"],
+                         specialize=specialize)
+
+    @classmethod
     def fused_regs(cls, src1: str, src2: str, d1: int, d2: int, regs1: int, regs2: int, grid: int = 0,
                    specialize: Optional["Image"] = None) -> "Module":
         """Per-interval register budgets: interval 1 runs with regs1, interval 2 with regs2

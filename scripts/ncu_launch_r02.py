@@ -25,9 +25,7 @@ order = []
 
 
 def build(sa, sb, c, img):
-    if c.get("interval_regs"):
-        return hf.Module.fused_regs(sa, sb, c["d1"], c["d2"], *c["interval_regs"], grid=c["grid"], specialize=img)
-    return hf.Module.fused(sa, sb, c["d1"], c["d2"], regcap=c["reg_cap"] or "off", grid=c["grid"], specialize=img)
+    return hf.Module.from_config(sa, sb, c, specialize=img)
 
 
 for r in d["results"]:

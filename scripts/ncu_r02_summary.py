@@ -58,7 +58,7 @@ def main():
         f = t["fused"]
         c = cfg[pair]
         if pair in {r["pair"] for r in detail["results"]}:
-            keep = {k: c[k] for k in ("d1", "d2", "reg_cap", "interval_regs", "grid")}
+            keep = {k: c.get(k) for k in ("d1", "d2", "reg_cap", "interval_regs", "grid", "split_grid")}
             traffic[pair] = {"config": keep, "dram_bytes": f["dram__bytes_read.sum"] + f["dram__bytes_write.sum"],
                              "read": f["dram__bytes_read.sum"], "write": f["dram__bytes_write.sum"],
                              "algorithmic_bytes": c["bytes"], "ncu_ns": f["gpu__time_duration.sum"]}

@@ -60,9 +60,10 @@ def main():
         wa, wb = P.MEMBERS[a].sizes["full"](), P.MEMBERS[b].sizes["full"]()
         img = hf.Image(wa.image).merge(hf.Image(wb.image))
         sa, sb = P.source("b200", P.MEMBERS[a].stem), P.source("b200", P.MEMBERS[b].stem)
-        m = hf.Module.fused(sa, sb, r["d1"], r["d2"], regcap=r["reg_cap"] or "off", grid=r["grid"], specialize=img)
+        m = hf.Module.from_config(sa, sb, r, specialize=img)
         text = sass(m)
-        summary[r["pair"]] = {"config": [r["grid"], r["d1"], r["d2"], r["reg_cap"]], **summarize(text)}
+        summary[r["pair"]] = {"config": [r["grid"], r["d1"], r["d2"], r["reg_cap"], r.get("split_grid")],
+                              **summarize(text)}
         blobs.append(f"==== fused {r['pair']} (grid {r['grid']}, {r['d1']}/{r['d2']}, cap {r['reg_cap']}) "
                      f"{m.entry} ====\n" + excerpt(text))
     for c in (detail.get("crypto") or {}).get("pairs", []):

@@ -25,10 +25,7 @@ def test_benched_fused_kernel_matches_oracle(gpu, pair):
     wa, wb = P.MEMBERS[a].sizes["full"](), P.MEMBERS[b].sizes["full"]()
     img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
     sa, sb = P.source("b200", P.MEMBERS[a].stem), P.source("b200", P.MEMBERS[b].stem)
-    if c.get("interval_regs"):
-        m = hf.Module.fused_regs(sa, sb, c["d1"], c["d2"], *c["interval_regs"], grid=c["grid"], specialize=img)
-    else:
-        m = hf.Module.fused(sa, sb, c["d1"], c["d2"], regcap=c["reg_cap"] or "off", grid=c["grid"], specialize=img)
+    m = hf.Module.from_config(sa, sb, c, specialize=img)
     m.run(img, c["grid"])
     img.download()
     for key, w in ((a, wa), (b, wb)):

@@ -98,3 +98,17 @@ def test_sm100_corpus_pairs_compile_for_sm100a(hf, corpus, a, b):
     rec = EMIT[f"{a}+{b}"]
     m = hf.Module.fused(corpus["kernels"][a], corpus["kernels"][b], rec["d1"], rec["d2"])
     assert len(m.cubin) > 1000 and m.info.threads == rec["d1"] + rec["d2"]
+
+
+def test_heterogeneous_grid_needs_a_barrier_free_second_member(hf):
+    """split_grid gives member 2 whole CTAs as sub-blocks: a member with barriers or shared memory
+    (Hist's per-block bins) cannot be split that way and is rejected at build time."""
+    import pytest
+    from paper_2007_01277_b200 import pairs as P
+    with pytest.raises(hf.HFuseError) as e:
+        hf.Module.fused_opts(P.source("b200", "maxpool"), P.source("b200", "histogram"), 512, 512, split_grid=4)
+    assert e.value.name == "InvalidArgument"
+    with pytest.raises(hf.HFuseError):  # d0 not a multiple of d2
+        hf.Module.fused_opts(P.source("b200", "batchnorm"), P.source("b200", "im2col"), 640, 384, split_grid=4)
+    m = hf.Module.fused_opts(P.source("b200", "batchnorm"), P.source("b200", "im2col"), 768, 256, split_grid=4)
+    assert "hf_b1 = min(4, (int)gridDim.x)" in m.source

@@ -52,3 +52,24 @@ def test_dynamic_interval_scheduling_matches_oracle(gpu, a, b, vgrid):
             for key, w in ((a, wa), (b, wb)):
                 r = CK.check_member(key, img.array, CK.member_expected(key, w.image))
                 assert r["ok"], (grid, launch, key, r)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("a,b,d1,d2,b1", [("bn", "im2col", 768, 256, 8), ("bn", "upsample", 896, 128, 8),
+                                          ("hist", "maxpool", 512, 512, 5), ("im2col", "upsample", 768, 256, 3)])
+def test_heterogeneous_grid_matches_oracle(gpu, a, b, d1, d2, b1):
+    """split_grid: blocks below B1 fused, blocks above member 2 only (d0/d2 sub-blocks); the
+    outputs equal the oracle for grids below, at and above B1."""
+    hf = gpu
+    wa, wb = P.MEMBERS[a].sizes["parity"](), P.MEMBERS[b].sizes["parity"]()
+    sa, sb = P.source("b200", P.MEMBERS[a].stem), P.source("b200", P.MEMBERS[b].stem)
+    img = hf.Image(wa.image).merge(hf.Image(wb.image))
+    m = hf.Module.fused_opts(sa, sb, d1, d2, split_grid=b1, grid=b1, specialize=img)
+    assert "hf_vg2" in m.source
+    for grid in (max(1, b1 - 2), b1, b1 + 7):
+        img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
+        m.run(img, grid)
+        img.download()
+        for key, w in ((a, wa), (b, wb)):
+            r = CK.check_member(key, img.array, CK.member_expected(key, w.image))
+            assert r["ok"], (grid, key, r)
