@@ -390,8 +390,12 @@ def split_candidates(hf, sa, sb, img, stream, args, natural=0):
     shapes = [(d0, d0 // k) for d0 in (1024, 768, 512) for k in (2, 4, 8) if d0 // k >= 64 and (d0 // k) % 32 == 0]
     specs = [(d0 - d2, d2, cap, b1) for d0, d2 in shapes for cap in (None, 32) for b1 in b1s]
 
+    import torch
+    device = torch.cuda.current_device()
+
     def build(spec):
         d1, d2, cap, b1 = spec
+        torch.cuda.set_device(device)  # worker threads start on device 0 without a current context
         try:
             return spec, hf.Module.fused_opts(sa, sb, d1, d2, regcap=cap or "off", split_grid=b1, grid=b1,
                                               specialize=img)

@@ -354,6 +354,8 @@ Module compile(const Sm100Kernel& k, std::optional<int> maxrreg, bool lineinfo) 
   if (!device_available()) return m;  // CPU hosts: compile-only (ptxas still ran)
   Driver& d = drv();
   HF_CUDA(cudaGetDevice(&m.device));
+  HF_CUDA(cudaFree(nullptr));  // this thread's current device's primary context becomes current
+                               // (a module built on a worker thread needs it for cuModuleLoadData)
   CUmodule mod;
   cu_check(d.moduleLoadData(&mod, m.cubin.data()), "cuModuleLoadData");
   CUfunction fn;
