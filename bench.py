@@ -399,10 +399,14 @@ def split_candidates(hf, sa, sb, img, stream, args, natural=0):
         try:
             return spec, hf.Module.fused_opts(sa, sb, d1, d2, regcap=cap or "off", split_grid=b1, grid=b1,
                                               specialize=img)
-        except hf.HFuseError:
-            return spec, None
+        except hf.HFuseError as e:
+            return spec, e
     with ThreadPoolExecutor(max_workers=8) as pool:
         mods = list(pool.map(build, specs))
+    errs = [m for _, m in mods if isinstance(m, hf.HFuseError)]
+    if errs:
+        print(f"split candidates: {len(errs)} of {len(mods)} failed to build, e.g. {errs[0]}", file=sys.stderr)
+    mods = [(s, None if isinstance(m, hf.HFuseError) else m) for s, m in mods]
     out = []
     for (d1, d2, cap, b1), m in mods:
         if m is None:
