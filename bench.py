@@ -354,9 +354,14 @@ def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3, natural=0):
     if args.split and split_member(sb):
         cands += split_candidates(hf, sa, sb, img, stream, args, natural)
     best = None
-    for cfg, _ in sorted(cands, key=lambda c: c[1])[:top]:
+    # the `top` fastest screened points of each family (static split, heterogeneous partition)
+    # re-timed on equal terms: a screen's noise must not hand one family all the final slots
+    finalists = []
+    for fam in (False, True):
+        finalists += sorted((c for c in cands if bool(c[0]["split_grid"]) == fam), key=lambda c: c[1])[:top]
+    for cfg, _ in finalists:
         m = build_fused(hf, sa, sb, cfg, img)
-        t = gtime(hf, "single", m, None, img, cfg["grid"], 0, stream, 10, 5)["mean_us"]
+        t = gtime(hf, "single", m, None, img, cfg["grid"], 0, stream, 20, 5)["mean_us"]
         if best is None or t < best[1]:
             best = (cfg, t)
         del m
