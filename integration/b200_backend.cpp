@@ -47,7 +47,7 @@ class B200Backend : public mkfuse::ProfilerBackend {
     hf_error e;
     int cap = c.reg_cap ? *c.reg_cap : HF_REGCAP_OFF;
     if (hf_profile(s1_.c_str(), s2_.c_str(), c.d1, c.d2, cap, img_, /*grid=*/0, /*warmup=*/3,
-                   /*reps=*/10, /*flush_l2=*/1, /*specialize=*/1, &ev, &e))
+                   /*reps=*/10, /*flush_l2=*/0, /*specialize=*/1, &ev, &e))
       mkfuse::fail(static_cast<mkfuse::ErrCode>(e.code - 1), e.message);  // same ordinals
     return mkfuse::EvalOutcome{ev.cycles, ev.occupancy, ev.utilization};  // cycles = ns
   }

@@ -485,11 +485,15 @@ int hf_profile(const char* src1, const char* src2, int d1, int d2, int regcap, h
                int reps, int flush_l2, int specialize, hf_eval* out, hf_error* err) {
   return guarded(err, [&] {
     hf::rt::Module m = build_fused(src1, src2, d1, d2, regcap, grid, 0, specialize ? img : nullptr);
-    hf::rt::Timing t =
-        hf::rt::time(hf::rt::Mode::Single, m, nullptr, img->img, grid, 0, warmup, reps, flush_l2 != 0, nullptr);
+    // flushed: per-repetition events after an L2 sweep (interquartile mean); steady (flush_l2 = 0):
+    // the graph protocol, `reps` back-to-back repetitions per graph, median of 5 samples
+    double us = flush_l2 ? hf::rt::time(hf::rt::Mode::Single, m, nullptr, img->img, grid, 0, warmup, reps, true,
+                                        nullptr).iqm_us
+                         : hf::rt::time_graph(hf::rt::Mode::Single, m, nullptr, img->img, grid, 0,
+                                              std::max(1, reps), 5).median_us;
     hf::rt::Props p = hf::rt::props();
-    out->us = t.iqm_us;
-    out->cycles = (long long)(t.iqm_us * 1000.0 + 0.5);
+    out->us = us;
+    out->cycles = (long long)(us * 1000.0 + 0.5);
     out->occupancy = double(m.blocks_per_sm) * (d1 + d2) / double(p.max_threads_per_sm);
     out->utilization = 0.0;
     out->regs = m.regs;

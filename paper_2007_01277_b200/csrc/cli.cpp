@@ -11,7 +11,8 @@
 //                      model ranks best, plus those predicted within F of the best; default 0.03)
 //   hfuse occupancy [K] [--regs N --shmem B --threads T] [--sm S]
 //   hfuse check K              hfuse lower K [-o F]           hfuse emit K [-o F]
-//   hfuse profile CANDIDATE(.cu|.mk) --mem IMG... [--grid G]   (mkfuse --profiler-cmd target)
+//   hfuse profile CANDIDATE(.cu|.mk) --mem IMG... [--grid G] [--reps N] [--no-flush]
+//                              (mkfuse --profiler-cmd target; --no-flush: steady graph protocol)
 //
 // Same flags, stdout keys and exit codes (0 ok; 1 + "error[Code] l:c: msg" on stderr).
 // `simulate` and `search` run on the GPU: the reference's cycle simulator is replaced by
@@ -43,7 +44,7 @@ struct Args {
   std::optional<uint64_t> seed;
   std::string sm = "pascal-like", regcap = "auto", style, out, trace, entry, profiler_cmd, dump, caps, iregs;
   bool sequential = false, sm_given = false, regcap_given = false, budgets = false;
-  bool launch_only = false, counters = true;
+  bool launch_only = false, counters = true, no_flush = false;
   int prefilter = 0;
   double prefilter_tol = -1.0;
   int d0 = 1024, d1 = 0, d2 = 0, regs = 0, threads = 0, granularity = 128, reps = 10, warmup = 3, grid = 0;
@@ -94,6 +95,7 @@ Args parse_args(int argc, char** argv) {
     else if (s == "--sequential") a.sequential = true;
     else if (s == "--launch-only") a.launch_only = true;  // internal: the ncu counter pass
     else if (s == "--no-counters") a.counters = false;
+    else if (s == "--no-flush") a.no_flush = true;
     else if (s == "--budgets") a.budgets = true;
     else if (s == "--regs") a.regs = num();
     else if (s == "--shmem") a.shmem = std::stoll(val());
@@ -433,9 +435,11 @@ int cmd_profile(const Args& a) {
     k = wrap_goto(text, a.grid);
   }
   rt::Module m = rt::compile(k, cap);
-  rt::Timing t = rt::time(rt::Mode::Single, m, nullptr, img, a.grid, 0, a.warmup, a.reps, true);
-  std::printf("%lld\n", (long long)(t.iqm_us * 1000.0 + 0.5));
-  std::printf("us = %.3f\nregisters = %d\nblocks_per_sm = %d\n", t.iqm_us, m.regs, m.blocks_per_sm);
+  // --no-flush: the steady graph protocol (back-to-back repetitions, median of 5 graph samples)
+  double us = a.no_flush ? rt::time_graph(rt::Mode::Single, m, nullptr, img, a.grid, 0, std::max(1, a.reps), 5).median_us
+                         : rt::time(rt::Mode::Single, m, nullptr, img, a.grid, 0, a.warmup, a.reps, true).iqm_us;
+  std::printf("%lld\n", (long long)(us * 1000.0 + 0.5));
+  std::printf("us = %.3f\nregisters = %d\nblocks_per_sm = %d\n", us, m.regs, m.blocks_per_sm);
   rt::unload(m);
   return 0;
 }

@@ -37,13 +37,14 @@ def test_reference_search_config_drives_b200(gpu, corpus, tmp_path):
     for stem in ("batchnorm", "histogram"):
         (tmp_path / f"{stem}.mk").write_text(corpus["kernels"][stem])
         (tmp_path / f"{stem}.img").write_text(corpus["images"][stem])
-    cmd = f"{EXE} profile --mem {tmp_path / 'batchnorm.img'} --mem {tmp_path / 'histogram.img'} --reps 20"
+    cmd = f"{EXE} profile --mem {tmp_path / 'batchnorm.img'} --mem {tmp_path / 'histogram.img'} --reps 20 --no-flush"
     r = subprocess.run([BIN, tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", tmp_path / "batchnorm.img",
                         tmp_path / "histogram.img", "--cmd", cmd], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr
     s = sections(r.stdout)
     img = hf.Image(corpus["images"]["batchnorm"]).merge(hf.Image(corpus["images"]["histogram"])).upload()
-    ours = hf.search(corpus["kernels"]["batchnorm"], corpus["kernels"]["histogram"], img, reps=10, specialize=True)
+    ours = hf.search(corpus["kernels"]["batchnorm"], corpus["kernels"]["histogram"], img, reps=10, specialize=True,
+                     flush_l2=False)
     us = {}  # d1 -> hfuse's best time over its caps (r0 comes from ptxas there, from the model here)
     for row in ours["trace"]:
         us[row["d1"]] = min(us.get(row["d1"], float("inf")), row["us"])
