@@ -36,7 +36,7 @@ def sass(m):
 
 
 def summarize(text):
-    body = [ln for ln in text.splitlines() if re.match(r"\s+/\*[0-9a-f]{4}\*/", ln)]
+    body = [ln for ln in text.splitlines() if re.match(r"\s+/\*[0-9a-f]{4,6}\*/", ln)]
     out = {k: sum(1 for ln in body if re.search(p, ln)) for k, p in PATTERNS.items()}
     out["instructions"] = len(body)
     for key, pat in (("regs", r"REG:(\d+)"), ("stack", r"STACK:(\d+)"), ("local", r"LOCAL:(\d+)")):
@@ -46,7 +46,7 @@ def summarize(text):
 
 
 def excerpt(text, keys=("LDG.E.128", "STG.E.128", "BAR.SYNC", "USETMAXREG", "ATOMS", "SHFL"), n=40):
-    lines = [ln for ln in text.splitlines() if re.match(r"\s+/\*[0-9a-f]{4}\*/", ln)]
+    lines = [ln for ln in text.splitlines() if re.match(r"\s+/\*[0-9a-f]{4,6}\*/", ln)]
     pick = [ln for ln in lines if any(re.search(PATTERNS[k], ln) for k in keys)]
     return "\n".join(pick[:n])
 
