@@ -5,6 +5,8 @@
 //   hfuse simulate K [--mem IMG]... [--seed S] [--regcap n|auto|off] [--dump-mem F] [--entry E]
 //   hfuse simulate --sequential K1 K2 --mem IMG... [--dump-mem F]
 //   hfuse search K1 K2 [--d0 N] --mem IMG... [--trace F] [-o F] [--style S] [--profiler-cmd CMD]
+//                      [--gpus N]  (time the sweep's candidates on N GPUs at once)
+//                      [--baseline seq|2stream|both]  (time the unfused members against the winner)
 //                      [--granularity G] [--caps 32,40,...] [--reps N] [--budgets]
 //                      (--budgets: also sweep per-interval setmaxnreg register budgets)
 //                      [--prefilter K [--prefilter-tol F]]  (time only the K partitions the B200
@@ -18,6 +20,7 @@
 // `simulate` and `search` run on the GPU: the reference's cycle simulator is replaced by
 // device execution (elapsed_us from CUDA events); `--sm` defaults to pascal-like for
 // `fuse`/`occupancy` (report parity) and to the live device for GPU commands.
+#include <cuda_runtime.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -45,6 +48,8 @@ struct Args {
   std::string sm = "pascal-like", regcap = "auto", style, out, trace, entry, profiler_cmd, dump, caps, iregs;
   bool sequential = false, sm_given = false, regcap_given = false, budgets = false;
   bool launch_only = false, counters = true, no_flush = false;
+  int gpus = 1;
+  std::string baseline;
   int prefilter = 0;
   double prefilter_tol = -1.0;
   int d0 = 1024, d1 = 0, d2 = 0, regs = 0, threads = 0, granularity = 128, reps = 10, warmup = 3, grid = 0;
@@ -96,6 +101,12 @@ Args parse_args(int argc, char** argv) {
     else if (s == "--launch-only") a.launch_only = true;  // internal: the ncu counter pass
     else if (s == "--no-counters") a.counters = false;
     else if (s == "--no-flush") a.no_flush = true;
+    else if (s == "--gpus") a.gpus = num();
+    else if (s == "--baseline") {
+      a.baseline = val();
+      if (a.baseline != "seq" && a.baseline != "2stream" && a.baseline != "both")
+        raise(Code::InvalidArgument, "--baseline takes seq, 2stream or both");
+    }
     else if (s == "--budgets") a.budgets = true;
     else if (s == "--regs") a.regs = num();
     else if (s == "--shmem") a.shmem = std::stoll(val());
@@ -357,6 +368,7 @@ int cmd_search(const Args& a) {
   }
   std::unique_ptr<ProfilerBackend> be;
   Image img;
+  std::vector<Image> imgs;  // --gpus N: one copy of the memory image per device
   SM sm = a.sm_given ? SM::preset_or_file(a.sm) : SM::b200();
   if (!a.profiler_cmd.empty()) {
     // budgets exist only in sm100 text, so a budget sweep (or --style sm100) hands the command
@@ -368,11 +380,43 @@ int cmd_search(const Args& a) {
     if (!a.sm_given) sm = rt::sm_from_device();
     img = images(a);
     rt::upload(img);
-    auto dev = std::make_unique<DeviceBackend>(img, a.grid, a.warmup, a.reps, true);
     std::map<std::string, ScalarVal> spec;
     for (const auto& [n, s] : img.scalars) spec[n] = ScalarVal{s.ty, s.i, s.f};
+    auto dev = std::make_unique<DeviceBackend>(img, a.grid, a.warmup, a.reps, true);
     dev->set_specialization(spec);  // JIT-specialize every candidate to the image's shapes
-    be = std::move(dev);
+    std::vector<int> want;  // devices of the sweep: 0 .. min(--gpus, count) - 1
+    for (int d = 0; d < std::min(a.gpus, rt::device_count()); ++d) want.push_back(d);
+    if (const char* e = std::getenv("HFUSE_SEARCH_DEVICES")) {  // test knob: an explicit id list
+      want.clear();
+      std::stringstream ss(e);
+      std::string t;
+      while (std::getline(ss, t, ',')) want.push_back(std::stoi(t));
+    }
+    int n = int(want.size());
+    if (n > 1) {
+      // the candidates of the sweep are timed on n GPUs at once (MultiDeviceBackend)
+      std::vector<std::unique_ptr<DeviceBackend>> devs;
+      std::vector<int> ids{want[0]};
+      int here = 0;
+      cudaGetDevice(&here);
+      devs.push_back(std::move(dev));
+      imgs.resize(size_t(n - 1));
+      for (int i = 1; i < n; ++i) {
+        int d = want[size_t(i)];
+        rt::set_device(d);
+        imgs[size_t(i - 1)] = images(a);
+        rt::upload(imgs[size_t(i - 1)]);
+        auto dd = std::make_unique<DeviceBackend>(imgs[size_t(i - 1)], a.grid, a.warmup, a.reps, true);
+        dd->set_specialization(spec);
+        devs.push_back(std::move(dd));
+        ids.push_back(d);
+      }
+      rt::set_device(here);
+      be = std::make_unique<MultiDeviceBackend>(std::move(devs), ids);
+    } else {
+      be = std::move(dev);
+    }
+    std::printf("devices = %d\n", std::max(1, n));
   }
   SearchResult r = (n1.tunable && n2.tunable) ? search_config(n1, n2, a.d0, *be, sm, so)
                                               : fixed_partition_fuse(n1, n2, *be, sm, a.d0, so);
@@ -391,6 +435,39 @@ int cmd_search(const Args& a) {
     Style st = style == "goto" ? Style::Goto : style == "sm100" ? Style::Sm100 : Style::Structured;
     write_text(a.out, emit(r.best, st));
     std::printf("wrote %s\n", a.out.c_str());
+  }
+  if (!a.baseline.empty()) {
+    // the unfused members at their declared dims against the best fused point, graph-timed on
+    // the (first) device: sequential a; b and/or two-stream a || b, and the speed-up over the
+    // faster of the requested baselines
+    if (!a.profiler_cmd.empty()) raise(Code::InvalidArgument, "--baseline needs the device backend");
+    std::map<std::string, ScalarVal> spec;
+    for (const auto& [n, s] : img.scalars) spec[n] = ScalarVal{s.ty, s.i, s.f};
+    Sm100Options o;
+    o.specialize = spec;
+    rt::Module m1 = rt::compile(emit_sm100(l1.kernel, l1.prog.funcs, o));
+    rt::Module m2 = rt::compile(emit_sm100(l2.kernel, l2.prog.funcs, o));
+    Sm100Options of;
+    of.specialize = spec;
+    rt::Module mf = rt::compile(emit_sm100(r.best, of), r.best_cfg.reg_cap);
+    int grid = a.grid > 0 ? a.grid : r.best.grid;
+    double tf = rt::time_graph(rt::Mode::Single, mf, nullptr, img, grid, 0, std::max(1, a.reps), 5).mean_us;
+    double base = 1e300;
+    std::printf("best_us = %.3f\n", tf);
+    if (a.baseline != "2stream") {
+      double t = rt::time_graph(rt::Mode::Sequential, m1, &m2, img, a.grid, a.grid, std::max(1, a.reps), 5).mean_us;
+      std::printf("sequential_us = %.3f\n", t);
+      base = std::min(base, t);
+    }
+    if (a.baseline != "seq") {
+      double t = rt::time_graph(rt::Mode::TwoStream, m1, &m2, img, a.grid, a.grid, std::max(1, a.reps), 5).mean_us;
+      std::printf("two_stream_us = %.3f\n", t);
+      base = std::min(base, t);
+    }
+    std::printf("speedup = %.4f\n", base / tf);
+    rt::unload(m1);
+    rt::unload(m2);
+    rt::unload(mf);
   }
   return 0;
 }

@@ -162,6 +162,16 @@ void randomize_phase(cudaStream_t s) {
 
 }  // namespace
 
+int device_count() {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
+
+void set_device(int device) {
+  HF_CUDA(cudaSetDevice(device));
+  HF_CUDA(cudaFree(nullptr));
+}
+
 bool device_available() {
   int n = 0;
   return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;

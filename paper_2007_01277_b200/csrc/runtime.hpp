@@ -48,6 +48,8 @@ struct Props {
 };
 
 Props props(int device = -1);
+int device_count();
+void set_device(int device);  // this host thread's current device (its primary context current)
 SM sm_from_device(int device = -1);
 bool device_available();
 

@@ -42,6 +42,11 @@ class ProfilerBackend {
   // Calibration for the model pre-filter: the time of one constituent run alone with `threads`
   // threads per block (partition_dims), or nullopt when the backend cannot measure it.
   virtual std::optional<double> member_time(const Kernel& k, int threads) { return std::nullopt; }
+  // Evaluates a whole sweep; entry i is candidate i's outcome or nullopt when it is infeasible
+  // (does not compile or fit). The default evaluates in order; MultiDeviceBackend spreads the
+  // candidates over several GPUs. The fold always consumes the results in candidate order.
+  virtual std::vector<std::optional<EvalOutcome>> evaluate_many(
+      const std::vector<std::pair<Fused, FusionConfig>>& candidates);
 };
 
 // Spawns `command <source-file>` and reads the first integer of its stdout (search.cpp:32-62).
@@ -75,6 +80,27 @@ class DeviceBackend : public ProfilerBackend {
   Image& img_;
   int grid_, warmup_, reps_;
   bool flush_, measured_;
+};
+
+// One DeviceBackend per GPU (each with its own copy of the memory image): evaluate_many times
+// disjoint candidates concurrently, one host thread per device pulling from a shared counter, so
+// an N-GPU box searches N times faster; the fold is unchanged (candidate order, strict <).
+// Every device must be the same model for the times to be comparable (checked at construction).
+class MultiDeviceBackend : public ProfilerBackend {
+ public:
+  MultiDeviceBackend(std::vector<std::unique_ptr<DeviceBackend>> devices, std::vector<int> ids);
+  EvalOutcome evaluate(const Fused& fused, const FusionConfig& cfg) override;
+  Resources resources(const Kernel& k, int threads) override;
+  void prepare(const std::vector<std::pair<Fused, FusionConfig>>& candidates) override;
+  bool supports_budgets() const override { return true; }
+  std::optional<double> member_time(const Kernel& k, int threads) override;
+  std::vector<std::optional<EvalOutcome>> evaluate_many(
+      const std::vector<std::pair<Fused, FusionConfig>>& candidates) override;
+  size_t size() const { return devs_.size(); }
+
+ private:
+  std::vector<std::unique_ptr<DeviceBackend>> devs_;
+  std::vector<int> ids_;
 };
 
 std::string cap_text(const FusionConfig& cfg);  // "none", "N" or "R1/R2" (budgets)

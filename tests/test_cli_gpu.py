@@ -109,3 +109,22 @@ def test_profile_command_with_sm100_candidates(gpu, corpus, tmp_path):
     assert r.returncode == 0, r.stderr
     rows = trace.read_text().splitlines()
     assert len(rows) == 15 and all(int(row.split(",")[3]) > 0 for row in rows[1:])
+
+
+@pytest.mark.gpu
+def test_search_on_several_devices_and_baselines(gpu, corpus, tmp_path):
+    """`search --gpus N` times the sweep's candidates on N devices at once (MultiDeviceBackend;
+    here two workers on device 0 through the HFUSE_SEARCH_DEVICES test knob, the only GPU of the
+    box): the same 14-point sweep and fold. `--baseline both` then times the unfused members
+    sequentially and on two streams against the winner."""
+    write_corpus(corpus, tmp_path)
+    env = dict(os.environ, HFUSE_SEARCH_DEVICES="0,0")
+    r = subprocess.run([EXE, "search", tmp_path / "batchnorm.mk", tmp_path / "histogram.mk", "--mem",
+                        tmp_path / "batchnorm.img", "--mem", tmp_path / "histogram.img", "--reps", "5",
+                        "--baseline", "both"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr
+    kv = dict(line.split(" = ") for line in r.stdout.strip().splitlines() if " = " in line)
+    assert kv["devices"] == "2" and kv["evaluated"] == "14"
+    assert float(kv["best_us"]) > 0 and float(kv["sequential_us"]) > 0 and float(kv["two_stream_us"]) > 0
+    assert abs(float(kv["speedup"]) - min(float(kv["sequential_us"]), float(kv["two_stream_us"])) /
+               float(kv["best_us"])) < 1e-3
