@@ -5,7 +5,7 @@
 #  3. --set full of the dominant fused kernel                          -> prof_dom_r02.ncu-rep
 mkdir -p gpurun_out
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,smsp__issue_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_elapsed,sm__warps_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread,smsp__inst_executed.sum,smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio,smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio,smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,launch__grid_size,launch__block_size
-timeout 1200 ncu --metrics $M --clock-control none -k regex:'^(bn_|hist|im2col|maxpool|upsample|fused|sha256d|blake|ethash)' --csv --log-file gpurun_out/ncu_r02.csv python scripts/ncu_launch_r02.py > gpurun_out/ncu_r02.order 2> gpurun_out/ncu_r02.err
+timeout 1200 ncu --metrics $M --clock-control none -k regex:'^(bn_|hist|im2col|maxpool|upsample|fused|sha256d|blake|ethash)' --csv --log-file gpurun_out/ncu_r02.csv python scripts/ncu_launch_r02.py --finalists > gpurun_out/ncu_r02.order 2> gpurun_out/ncu_r02.err
 echo "metrics_rc=$?" >> gpurun_out/ncu_r02.err
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "step/" \
   --csv --log-file gpurun_out/launches_r02.csv python bench.py --steps 3 --warmup 3 --no-crypto --no-cpu-baseline --no-parity --no-ceilings --detail gpurun_out/launch_bench_detail.json \

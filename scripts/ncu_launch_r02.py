@@ -18,6 +18,8 @@ ap.add_argument("--detail", default=os.path.join(ROOT, "profiles", "r02_bench_de
 ap.add_argument("--only", default="", help="comma list of pairs (default all)")
 ap.add_argument("--fused-only", action="store_true")
 ap.add_argument("--no-crypto", action="store_true")
+ap.add_argument("--finalists", action="store_true",
+                help="also launch every re-timed finalist configuration of the search (trace 'final' rows)")
 args = ap.parse_args()
 d = json.load(open(args.detail))
 only = set(args.only.split(",")) if args.only else None
@@ -40,6 +42,12 @@ for r in d["results"]:
             order.append(f"{r['pair']}:{k}")
     build(sa, sb, r, img).run(img, r["grid"])
     order.append(f"{r['pair']}:fused")
+    if args.finalists:
+        keys = ("d1", "d2", "reg_cap", "interval_regs", "split_grid", "grid")
+        for row in d["search"].get(r["pair"], []):
+            if row[0] == "final" and {k: row[1].get(k) for k in keys} != {k: r.get(k) for k in keys}:
+                build(sa, sb, row[1], img).run(img, row[1]["grid"])
+                order.append(f"{r['pair']}:final:" + json.dumps({k: row[1].get(k) for k in keys}))
     del img
 if not args.no_crypto:
     for c in d["crypto"]["pairs"]:

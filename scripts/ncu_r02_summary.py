@@ -46,8 +46,12 @@ def main():
     cfg = {r["pair"]: r for r in detail["results"]}
     cfg.update({c["pair"]: c for c in detail["crypto"]["pairs"]})
     table = OrderedDict()
+    finals = OrderedDict()  # pair -> [(config, metrics)] of the search's other finalists
     for label, ((_, name), m) in zip(order, launches):
-        pair, role = label.split(":")
+        pair, role = label.split(":", 1)
+        if role.startswith("final:"):
+            finals.setdefault(pair, []).append((json.loads(role[len("final:"):]), dict(kernel=name, **m)))
+            continue
         table.setdefault(pair, {})[role] = dict(kernel=name, **m)
     json.dump({"how": "scripts/gpu_ncu_r02.sh: ncu --metrics ... --clock-control none over scripts/ncu_launch_r02.py "
                       "(benched configurations of profiles/r02_bench_detail.json, each pair on its own tensors)",
@@ -59,9 +63,11 @@ def main():
         c = cfg[pair]
         if pair in {r["pair"] for r in detail["results"]}:
             keep = {k: c.get(k) for k in ("d1", "d2", "reg_cap", "interval_regs", "grid", "split_grid")}
-            traffic[pair] = {"config": keep, "dram_bytes": f["dram__bytes_read.sum"] + f["dram__bytes_write.sum"],
-                             "read": f["dram__bytes_read.sum"], "write": f["dram__bytes_write.sum"],
-                             "algorithmic_bytes": c["bytes"], "ncu_ns": f["gpu__time_duration.sum"]}
+            rows = [(keep, f)] + finals.get(pair, [])
+            traffic[pair] = [{"config": cf, "dram_bytes": mm["dram__bytes_read.sum"] + mm["dram__bytes_write.sum"],
+                              "read": mm["dram__bytes_read.sum"], "write": mm["dram__bytes_write.sum"],
+                              "algorithmic_bytes": c["bytes"], "ncu_ns": mm["gpu__time_duration.sum"]}
+                             for cf, mm in rows]
         a, b = pair.split("+")
         ia, ib = t[a], t[b]
         key = "smsp__issue_active.avg.pct_of_peak_sustained_elapsed"
