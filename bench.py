@@ -146,8 +146,7 @@ def run_reference_arm(args):
     Every step runs the ten naive pairs at full C2 size through run_functional (k1 then k2),
     each pair split into REF_SHARDS batch shards (exact slices of the whole-batch tensors), the
     jobs spread over all host cores. Nothing from the product (libhfuse.so) is loaded. Warm-up
-    steps run one shard per pair: an interpreter process keeps no state from one run to the next
-    (only the page cache of its binary and inputs warms up)."""
+    steps are whole steps too (untimed)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -163,9 +162,8 @@ def run_reference_arm(args):
     reps = world if args.scaling == "weak" else 1   # weak scaling: the job is N whole workloads
     with tempfile.TemporaryDirectory() as d:
         jobs = ref_jobs(pair_list, shape, REF_SHARDS, d) * reps
-        warm = ref_jobs(pair_list, shape, REF_SHARDS, d, which=[0])
         for _ in range(args.warmup):
-            run_jobs(warm, nproc)
+            run_jobs(jobs, nproc)
         t0 = time.perf_counter()
         for _ in range(args.steps):
             run_jobs(jobs, nproc)
@@ -177,7 +175,7 @@ def run_reference_arm(args):
         "scaling": args.scaling, "vs_baseline": None, "dtype": "fp32/int32", "data": "synthetic (seeded splitmix64)",
         "config": {"workload": f"C2: 10 DL pairs (naive member forms) at full size, run_functional k1;k2"
                                + (f" x{reps} (weak)" if reps > 1 else ""),
-                   "shards_per_pair": REF_SHARDS, "warmup": "1 shard per pair"},
+                   "shards_per_pair": REF_SHARDS},
         "cpu_baseline": {"value": round(us), "unit": "us", "cores": nproc, "kind": "reference", "nproc": nproc,
                          "cpu_model": model,
                          "sample": f"whole workload: {len(jobs)} mkfuse_ref jobs per step over {nproc} threads"},
