@@ -63,11 +63,11 @@ def main():
         c = cfg[pair]
         if pair in {r["pair"] for r in detail["results"]}:
             keep = {k: c.get(k) for k in ("d1", "d2", "reg_cap", "interval_regs", "grid", "split_grid")}
-            rows = [(keep, f)] + finals.get(pair, [])
+            measured = [(keep, f)] + finals.get(pair, [])
             traffic[pair] = [{"config": cf, "dram_bytes": mm["dram__bytes_read.sum"] + mm["dram__bytes_write.sum"],
                               "read": mm["dram__bytes_read.sum"], "write": mm["dram__bytes_write.sum"],
                               "algorithmic_bytes": c["bytes"], "ncu_ns": mm["gpu__time_duration.sum"]}
-                             for cf, mm in rows]
+                             for cf, mm in measured]
         a, b = pair.split("+")
         ia, ib = t[a], t[b]
         key = "smsp__issue_active.avg.pct_of_peak_sustained_elapsed"
