@@ -391,7 +391,9 @@ def split_candidates(hf, sa, sb, img, stream, args, natural=0):
     Modules are NVRTC-compiled on a thread pool, then timed like the static points."""
     from concurrent.futures import ThreadPoolExecutor
     b1s = [natural] if natural else [296, 592, 1184]
-    shapes = [(d0, d0 // k) for d0 in (1024, 768, 512) for k in (2, 4, 8) if d0 // k >= 64 and (d0 // k) % 32 == 0]
+    # d2 = d0/2, d0/4, d0/8 and one warp (the fused blocks almost all member 1)
+    shapes = sorted({(d0, d0 // k) for d0 in (1024, 768, 512) for k in (2, 4, 8) if d0 // k >= 64 and (d0 // k) % 32 == 0}
+                    | {(d0, 32) for d0 in (1024, 768, 512)})
     specs = [(d0 - d2, d2, cap, b1) for d0, d2 in shapes for cap in (None, 32) for b1 in b1s]
 
     import torch
