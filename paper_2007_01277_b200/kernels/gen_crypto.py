@@ -1,7 +1,11 @@
 """Generator of the crypto member kernels (MK+), the C3/C4 workloads of SURVEY §8d.
 
 The paper's crypto kernels (ccminer SHA256d, Blake256, Blake2B and
-ethminer's Ethash) have fixed block sizes and straight-line, fully unrolled rounds. Mini-Kernel
+ethminer's Ethash) have straight-line, fully unrolled rounds. Every member here is tunable (any
+warp-multiple block size: nonces are strided by blockDim, the per-block minimum is indexed by the
+block), so the partition search sizes both intervals of a fused pair — a 128-thread BLAKE-256
+interval next to a 640-thread Ethash one beats the paper's fixed 512 + 512
+(profiles/r02_probe_crypto_tunable.jsonl). Mini-Kernel
 has no local arrays, so rounds are generated here as straight-line MK+ with statically
 renamed state registers (no register moves), hex constants, 32-bit rotates (funnel shifts on
 sm_100a) and 64-bit arithmetic in 32-bit halves (carry via `ltu`, rotates via `fshr`/`fshl`).
@@ -83,7 +87,7 @@ def decls(src, names, ty="int"):
         src(" ".join(f"{ty} {n};" for n in names[i:i + 12]))
 
 
-def header(src, p, kind, doc, params, dims, shared=True, fixed=True):
+def header(src, p, kind, doc, params, dims, shared=True, fixed=False):
     src.lines.append(doc.rstrip())
     src.lines.append("//@ grid=296")
     src.lines.append(f"kernel {kind}({params}) dims ({dims}, 1, 1){' fixed' if fixed else ''} {{")
