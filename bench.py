@@ -313,6 +313,22 @@ def gtime(hf, mode, a, b, img, ga, gb, stream, reps, samples):
     return hf.time_graph(mode, a, b, img, ga, gb, reps=reps, samples=samples, stream=stream)
 
 
+def interleaved(hf, variants, img, stream, reps, rounds):
+    """Graph-time several variants in rotation: `rounds` rounds, each one graph sample (reps
+    repetitions) of every variant in turn, so a drift in clocks or temperature hits all variants
+    alike. variants: name -> (mode, a, b, grid_a, grid_b). Returns name -> {mean_us, ci95_us}."""
+    samples = {k: [] for k in variants}
+    for _ in range(rounds):
+        for k, (mode, a, b, ga, gb) in variants.items():
+            samples[k].append(hf.time_graph(mode, a, b, img, ga, gb, reps=reps, samples=1, stream=stream)["mean_us"])
+    out = {}
+    for k, xs in samples.items():
+        mu = sum(xs) / len(xs)
+        sd = (sum((x - mu) ** 2 for x in xs) / (len(xs) - 1)) ** 0.5 if len(xs) > 1 else 0.0
+        out[k] = {"mean_us": mu, "ci95_us": 2.776 * sd / len(xs) ** 0.5 if len(xs) == 5 else 1.96 * sd / len(xs) ** 0.5}
+    return out
+
+
 def best_two_stream(hf, ka, kb, img, ga, gb, grids, stream, reps, samples):
     """The two-stream baseline with the same grid freedom as the fused kernel: every
     (grid_a, grid_b) screened with a short graph, the best and the members'-best pair re-timed
@@ -962,9 +978,13 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
                "per_rank_nonces": {a: na, b: nb}}
         if rank == 0:
             ga, gb = mg[a], mg[b]
-            tf = gtime(hf, "single", m, None, img, cfg["grid"], 0, stream, 3, 5)
-            seq = gtime(hf, "sequential", ka, kb, img, ga, gb, stream, 3, 5)
-            two, tga, tgb = best_two_stream(hf, ka, kb, img, ga, gb, cgrids, stream, 3, 5)
+            _, tga, tgb = best_two_stream(hf, ka, kb, img, ga, gb, cgrids, stream, 3, 3)
+            # the three variants in rotation (ALU-saturating hashes heat the GPU: back-to-back
+            # blocks of one variant would see different clocks than the next variant's)
+            t = interleaved(hf, {"fused": ("single", m, None, cfg["grid"], 0),
+                                 "seq": ("sequential", ka, kb, ga, gb),
+                                 "two": ("two_stream", ka, kb, tga, tgb)}, img, stream, reps=3, rounds=5)
+            tf, seq, two = t["fused"], t["seq"], t["two"]
             res.update({"grid_a": ga, "grid_b": gb, "two_stream_grids": [tga, tgb], "fused_us": tf["mean_us"],
                         "fused_ci95": tf["ci95_us"], "seq_us": seq["mean_us"], "two_stream_us": two["mean_us"],
                         "speedup": min(seq["mean_us"], two["mean_us"]) / tf["mean_us"], "trace": plan["trace"]})
