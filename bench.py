@@ -325,7 +325,8 @@ def interleaved(hf, variants, img, stream, reps, rounds):
     for k, xs in samples.items():
         mu = sum(xs) / len(xs)
         sd = (sum((x - mu) ** 2 for x in xs) / (len(xs) - 1)) ** 0.5 if len(xs) > 1 else 0.0
-        out[k] = {"mean_us": mu, "ci95_us": 2.776 * sd / len(xs) ** 0.5 if len(xs) == 5 else 1.96 * sd / len(xs) ** 0.5}
+        t95 = [12.706, 4.303, 3.182, 2.776, 2.571, 2.447, 2.365, 2.306, 2.262][len(xs) - 2] if 1 < len(xs) < 11 else 1.96
+        out[k] = {"mean_us": mu, "ci95_us": t95 * sd / len(xs) ** 0.5}
     return out
 
 
