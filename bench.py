@@ -1048,7 +1048,12 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
         if best is None or t["mean_us"] < best[1]["mean_us"]:
             best = (cand, t)
         del m
-    cand, tf = best
+    cand, _ = best
+    m = build_fused(hf, su, srcs["blake256"], cand, img)
+    t = interleaved(hf, {"fused": ("single", m, None, cand["grid"], 0), "seq": ("sequential", ku, kb, gu, gbk),
+                         "two": ("two_stream", ku, kb, tx, ty)}, img, stream, reps=10, rounds=7)
+    tf, seq, two = t["fused"], t["seq"], t["two"]
+    del m
     base = min(seq["mean_us"], two["mean_us"])
     c4 = {"pair": "upsample+blake256", **cand, "fused_us": tf["mean_us"], "fused_ci95": tf["ci95_us"],
           "seq_us": seq["mean_us"], "two_stream_us": two["mean_us"], "grid_a": gu, "grid_b": gbk,
