@@ -67,7 +67,7 @@ configuration.
 
 """)
     ops = load("crypto_ops.json")
-    c = replace_block(c, "**C3 — the paper's six crypto pairs**", "Five of six pairs win", f"""**C3 — the paper's six crypto pairs** (issue bound = source operations per nonce ×
+    c = replace_block(c, "**C3 — the paper's six crypto pairs**", "<!-- crypto-prose -->", f"""**C3 — the paper's six crypto pairs** (issue bound = source operations per nonce ×
 nonces / 32 / (148 SMs × 4 schedulers × f), `profiles/crypto_ops.json`; HBM bound = 8 KiB of
 DAG per Ethash nonce at the copy bandwidth; frac = the larger bound / fused time):
 
@@ -87,7 +87,8 @@ DAG per Ethash nonce at the copy bandwidth; frac = the larger bound / fused time
         ti = sum(n[k] * ops[k]["ops_per_nonce"] / 32 for k in (a, b)) / slots * 1e6
         return max(ti, n.get("ethash", 0) * 8192 / (6558.7 * 1e3)) / p["fused_us"]
     ef = [cfrac(p) for p in eth]
-    c = replace_block(c, "Five of six pairs win", "**The ALU pipe is the crypto pairs' real ceiling.**", f"""{len(cwins)} of {len(cr)} pairs win, by {min(p['speedup'] for p in cwins) * 100 - 100:.1f}–{max(p['speedup'] for p in cwins) * 100 - 100:.1f} %, {nbud} of them with per-interval
+    c = replace_block(c, "<!-- crypto-prose -->", "**The ALU pipe is the crypto pairs' real ceiling.**", f"""<!-- crypto-prose -->
+{len(cwins)} of {len(cr)} pairs win, by {min(p['speedup'] for p in cwins) * 100 - 100:.1f}–{max(p['speedup'] for p in cwins) * 100 - 100:.1f} %, {nbud} of them with per-interval
 `setmaxnreg` budgets{'; below: ' + ', '.join(closs) + ' (two ALU-pipe-bound hashes)' if closs else ''}. All four hashes are tunable, so
 the search also sizes the hash interval (e.g. a 128-thread BLAKE-256 interval beside a 640-thread
 Ethash one). The Ethash pairs sit at {min(ef):.2f}–{max(ef):.2f} of their bound: Ethash alone reads its random
