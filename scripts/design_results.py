@@ -187,6 +187,8 @@ C2 step on the box's {ref['cpu_baseline']['nproc']} cores (160 interpreter jobs 
 {line['e2e']['value'] / 1000:.1f} ms.
 
 """)
+    c = re.sub(r"\(`combined_utilization`\) in \d+ of \d+ pairs and above both members in \d+ \(§10\)",
+               f"(`combined_utilization`) in {ncomb} of {len(issue)} pairs and above both members in {nboth} (§10)", c)
     open(path, "w").write(c)
     print("DESIGN §10 regenerated:", line["value"], line["speedup_geomean"], f"{wins}/10", f"{ncomb}/{nboth}")
 
