@@ -553,9 +553,12 @@ def main():
         for i, (a, b) in enumerate(pair_list):
             c, m, img = cfgs[i], fused[i], imgs[i]
             ga, gb = mgrid[a], mgrid[b]
-            fz = gtime(hf, "single", m, None, img, c["grid"], 0, stream, R, S)
-            seq = gtime(hf, "sequential", unfused[a], unfused[b], img, ga, gb, stream, R, S)
-            two, tga, tgb = best_two_stream(hf, unfused[a], unfused[b], img, ga, gb, grids, stream, R, S)
+            _, tga, tgb = best_two_stream(hf, unfused[a], unfused[b], img, ga, gb, grids, stream, R, 3)
+            # the three variants of the comparison in rotation, S rounds of R repetitions each
+            t3 = interleaved(hf, {"fused": ("single", m, None, c["grid"], 0),
+                                  "seq": ("sequential", unfused[a], unfused[b], ga, gb),
+                                  "two": ("two_stream", unfused[a], unfused[b], tga, tgb)}, img, stream, R, S)
+            fz, seq, two = t3["fused"], t3["seq"], t3["two"]
             ta = gtime(hf, "single", unfused[a], None, img, ga, 0, stream, R, 3)
             tb = gtime(hf, "single", unfused[b], None, img, gb, 0, stream, R, 3)
             base = min(seq["mean_us"], two["mean_us"])
