@@ -876,12 +876,35 @@ ETHASH_PAGES = 33554393  # 4.3 GB synthetic DAG (>> the 126 MB L2): the largest 
                          # walked with Ethash's modulo rule (a real DAG's page count is prime too)
 
 
-def crypto_roofline(nonces, t_us, sm_mhz, hbm_peak):
+RP_GROUPS = 1 << 17  # random-page ceiling: 2^17 groups x 64 rounds x 8 pages x 128 B = 8.6 GB (one Ethash pair's DAG bytes)
+
+
+def dag_page_ceiling(hf, P, img, stream):
+    """HBM ceiling for Ethash's access pattern, measured on the pair's own DAG: independent,
+    well-mixed random 128-byte pages (kernels/probe/dag_pages.mk), 8 in flight per lane, best of
+    three launch shapes. The copy bandwidth is a sequential figure no random 128-B walk reaches
+    (profiles/r02_probe_random2.jsonl: 4.5-5.5 TB/s)."""
+    src = open(os.path.join(P.KERNELS, "probe", "dag_pages.mk")).read()
+    k = hf.Module.kernel(src, grid=1184, specialize=img)
+    nbytes = RP_GROUPS * 64 * 8 * 128
+    best = None
+    for g in (592, 1184, 2368):
+        t = gtime(hf, "single", k, None, img, g, 0, stream, 3, 3)["mean_us"]
+        if best is None or t < best[0]:
+            best = (t, g)
+    del k
+    return {"gbs": nbytes / (best[0] * 1e3), "us": best[0], "grid": best[1], "bytes": nbytes,
+            "kernel": "kernels/probe/dag_pages.mk"}
+
+
+def crypto_roofline(nonces, t_us, sm_mhz, hbm_peak, dag_gbs=None):
     """Pair roofline of SURVEY.md §8d: max(issue time, HBM time). Issue time = warp
     instructions / (148 SMs x 4 schedulers x f_sm) with each member's 32-bit operations per nonce
     counted from its kernel SOURCE (profiles/crypto_ops.json, scripts/crypto_ops.py: one
     instruction per source operation, a fixed algorithmic table, independent of what any compiled
-    kernel executes). HBM time: Ethash reads 64 pages x 128 B per nonce."""
+    kernel executes). HBM time: Ethash reads 64 pages x 128 B per nonce, at the copy bandwidth
+    (hbm_us) and, when measured, at the random-page ceiling of its DAG (hbm_random_us, which
+    then sets the bound: a random 128-B walk cannot stream at the copy figure)."""
     path = os.path.join(ROOT, "profiles", "crypto_ops.json")
     if not os.path.exists(path) or not sm_mhz:
         return None
@@ -891,10 +914,15 @@ def crypto_roofline(nonces, t_us, sm_mhz, hbm_peak):
     slots = 148 * 4 * sm_mhz * 1e6
     winst = sum(n * table[k]["ops_per_nonce"] / 32.0 for k, n in nonces.items())
     t_issue = winst / slots * 1e6
-    t_hbm = sum(n * 64 * 128 for k, n in nonces.items() if k == "ethash") / (hbm_peak * 1e3)
-    t_roof = max(t_issue, t_hbm)
-    return {"bound": "issue" if t_issue >= t_hbm else "hbm", "roofline_us": t_roof, "frac": t_roof / t_us,
-            "issue_us": t_issue, "hbm_us": t_hbm, "warp_inst": winst, "sm_mhz": sm_mhz}
+    dag = sum(n * 64 * 128 for k, n in nonces.items() if k == "ethash")
+    t_hbm = dag / (hbm_peak * 1e3)
+    t_mem = dag / (dag_gbs * 1e3) if dag_gbs else t_hbm
+    t_roof = max(t_issue, t_mem)
+    r = {"bound": "issue" if t_issue >= t_mem else "hbm", "roofline_us": t_roof, "frac": t_roof / t_us,
+         "issue_us": t_issue, "hbm_us": t_hbm, "warp_inst": winst, "sm_mhz": sm_mhz}
+    if dag_gbs:
+        r.update({"hbm_random_us": t_mem, "dag_ceiling_gbs": dag_gbs, "frac_copy_hbm": t_hbm / t_us})
+    return r
 
 
 def crypto_parity(hf, CR, sa, sb, a, b, cfg, threads_b):
@@ -930,24 +958,39 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
     from paper_2007_01277_b200 import pairs as P
     from paper_2007_01277_b200 import shard as SH
     rank, world = D.rank, D.world
-    cgrids = [296, 592]
     srcs = {k: open(os.path.join(P.KERNELS, "b200", k + ".mk")).read() for k in CR.MEMBERS}
+    # every source form of a member (Ethash: the lean fused member and the register form, faster
+    # alone): the unfused baselines run each member's fastest (form, grid)
+    forms = {k: {f: open(os.path.join(P.KERNELS, "b200", f + ".mk")).read() for f in CR.FORMS[k]}
+             for k in CR.MEMBERS}
     out = {"pairs": [], "parity_ok": True}
+    dag_ceiling = None
     for a, b in CRYPTO_PAIRS:
+        cgrids = [148, 296, 592] if b == "ethash" else [296, 592]
         na0, na = SH.nonce_slice(CRYPTO_COUNTS[a], rank, world)
         nb0, nb = SH.nonce_slice(CRYPTO_COUNTS[b], rank, world)
         gmax = max(cgrids)
         wa = CR.workload(a, na, gmax, nonce0=na0, target=1 << 12)
         wb = CR.workload(b, nb, gmax, nonce0=nb0, target=1 << 12, npages=ETHASH_PAGES)
-        img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload(stream)
-        ka = hf.Module.kernel(srcs[a], grid=cgrids[0], specialize=img)
-        kb = hf.Module.kernel(srcs[b], grid=cgrids[0], specialize=img)
+        img = hf.Image(wa.image).merge(hf.Image(wb.image))
+        if b == "ethash":
+            img = img.merge(hf.Image(f"array rp_sink int32 4 zero\nscalar rp_groups int32 {RP_GROUPS}\n"))
+        img = img.upload(stream)
         plan = None
         if rank == 0:
-            mg = {}
-            for name, k in ((a, ka), (b, kb)):
-                ts = {g: gtime(hf, "single", k, None, img, g, 0, stream, 2, 3)["mean_us"] for g in cgrids}
-                mg[name] = min(ts, key=ts.get)
+            if b == "ethash" and dag_ceiling is None:
+                dag_ceiling = dag_page_ceiling(hf, P, img, stream)
+            mg, base = {}, {}
+            for name in (a, b):
+                best_alone = None
+                for form, fsrc in forms[name].items():
+                    k = hf.Module.kernel(fsrc, grid=cgrids[0], specialize=img)
+                    for g in cgrids:
+                        t = gtime(hf, "single", k, None, img, g, 0, stream, 2, 3)["mean_us"]
+                        if best_alone is None or t < best_alone[0]:
+                            best_alone = (t, g, form)
+                    del k
+                mg[name], base[name] = best_alone[1], best_alone[2]
             best, traces = None, []
             for g in cgrids:
                 for d0 in ((1024,) if b != "ethash" else (768, 896, 1024)):
@@ -974,7 +1017,7 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
                 if best is None or t < best[1]:
                     best = (cfg, t)
                 del mm
-            plan = {"mg": mg, "cfg": best[0], "trace": traces}
+            plan = {"mg": mg, "base": base, "cfg": best[0], "trace": traces}
         plan = D.bcast(plan)
         cfg, mg = plan["cfg"], plan["mg"]
         m = build_fused(hf, srcs[a], srcs[b], cfg, img)
@@ -982,6 +1025,9 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
                "per_rank_nonces": {a: na, b: nb}}
         if rank == 0:
             ga, gb = mg[a], mg[b]
+            res["baseline_forms"] = plan["base"]
+            ka = hf.Module.kernel(forms[a][plan["base"][a]], grid=cgrids[0], specialize=img)
+            kb = hf.Module.kernel(forms[b][plan["base"][b]], grid=cgrids[0], specialize=img)
             _, tga, tgb = best_two_stream(hf, ka, kb, img, ga, gb, cgrids, stream, 3, 3)
             # the three variants in rotation (ALU-saturating hashes heat the GPU: back-to-back
             # blocks of one variant would see different clocks than the next variant's)
@@ -992,9 +1038,11 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
             res.update({"grid_a": ga, "grid_b": gb, "two_stream_grids": [tga, tgb], "fused_us": tf["mean_us"],
                         "fused_ci95": tf["ci95_us"], "seq_us": seq["mean_us"], "two_stream_us": two["mean_us"],
                         "speedup": min(seq["mean_us"], two["mean_us"]) / tf["mean_us"], "trace": plan["trace"]})
-            res["roofline"] = crypto_roofline({a: na, b: nb}, tf["mean_us"], sm_mhz, hbm_peak)
+            res["roofline"] = crypto_roofline({a: na, b: nb}, tf["mean_us"], sm_mhz, hbm_peak,
+                                              dag_gbs=dag_ceiling["gbs"] if b == "ethash" and dag_ceiling else None)
             if b == "ethash":
                 res["dag_gbs_fused"] = nb * 64 * 128 / (tf["mean_us"] * 1e3)
+            del ka, kb
         # the single exchange: hits + winning nonce of both members over all ranks
         img.upload(stream)
         m.run(img, cfg["grid"], stream)
@@ -1014,7 +1062,8 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
             res["parity_ok"] = crypto_parity(hf, CR, srcs[a], srcs[b], a, b, cfg, cfg["d2"])
             out["parity_ok"] &= res["parity_ok"]
         out["pairs"].append(res)
-        del m, ka, kb, img
+        del m, img
+    out["dag_ceiling"] = dag_ceiling
     if rank != 0:
         return out
     # C4: Upsample + Blake256, every variant at its best grid

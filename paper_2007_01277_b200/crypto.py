@@ -7,7 +7,11 @@ from dataclasses import dataclass
 from typing import List, Optional
 
 MEMBERS = {"sha256d": "sh", "blake256": "bl", "blake2b": "b2", "ethash": "eh"}
-THREADS = {"sha256d": 512, "blake256": 512, "blake2b": 512, "ethash": 256}
+THREADS = {"sha256d": 512, "blake256": 512, "blake2b": 512, "ethash": 1024}
+# member source files per kind: ethash.mk is the lean-register form (the fused member),
+# ethash_reg.mk the register form (faster alone; the bench's unfused baselines may run it)
+FORMS = {"sha256d": ["sha256d"], "blake256": ["blake256"], "blake2b": ["blake2b"], "ethash": ["ethash", "ethash_reg"]}
+FORM_THREADS = {"ethash_reg": 256}
 # Genesis block header (Bitcoin), the SHA-256d known-answer vector, as 20 big-endian words.
 GENESIS_HEADER = bytes.fromhex(
     "01000000" + "00" * 32 + "3ba3edfd7a7b12b27ac72c3e67768f617fc81bc3888a51323a9fb8aa4b1e5e4a"

@@ -63,6 +63,15 @@ HPP = int(os.environ.get("HF_ETHASH_HPP", "8"))  # Ethash: nonces of an 8-lane g
 # per-thread shared-memory ring (MK+ async_copy / async_wait), so no register holds a page in flight
 ETHASH_LOAD = os.environ.get("HF_ETHASH_LOAD", "ldg")
 ETHASH_TMAX = 512  # async form: the shared ring is sized for intervals of up to 512 threads
+# "lean" form: cp.async DAG ring + the Keccak-512 seed parked in shared memory across the DAG walk,
+# so the walk holds only the mixes (32 registers) and the page indices: twice the resident warps
+# (pages in flight) of the register form. Its shared arrays are sized for intervals of up to
+# ETHASH_LEAN_TMAX threads (8 x 16 B ring + 64 B seed per thread).
+# The lean form is the default member (every Ethash pair fuses 5-13 % faster with it, r02 probe);
+# the register form (ethash_reg.mk) is kept because it is ~5 % faster ALONE: the bench's unfused
+# baselines run whichever form is faster, so a fused win is never a win over a slowed member.
+ETHASH_FORM = os.environ.get("HF_ETHASH_FORM", "lean")
+ETHASH_LEAN_TMAX = int(os.environ.get("HF_ETHASH_TMAX", "1024"))
 ROT = [[0, 36, 3, 41, 18], [1, 44, 10, 45, 2], [62, 6, 43, 15, 61], [28, 55, 25, 21, 56], [27, 20, 39, 8, 14]]
 
 
@@ -490,6 +499,8 @@ def bcast8(src, var, lane_src, tmp="bt"):
 
 
 def gen_ethash():
+    if ETHASH_FORM == "lean":
+        return gen_ethash_lean()
     p = "eh"
     s = Src()
     hp = ", ".join(f"int {p}_h{i}" for i in range(8))
@@ -614,10 +625,135 @@ def gen_ethash():
     return s.text()
 
 
+def gen_ethash_lean():
+    """The same Ethash search as gen_ethash (identical outputs), laid out for memory-level
+    parallelism: the DAG walk of an 8-lane group's 8 nonces keeps only the mixes in registers
+    (lane j: words 4j..4j+3 of each, 32 registers); pages land in a per-thread shared ring through
+    16-byte cp.async copies (no register per page in flight) and the Keccak-512 seed waits in
+    shared memory (stride TMAX+1: conflict-free owner writes and group reads) until the final
+    Keccak-256. Block size = TMAX (the search may give its interval fewer threads)."""
+    p = "eh"
+    T = ETHASH_LEAN_TMAX
+    S = T + 1
+    s = Src()
+    hp = ", ".join(f"int {p}_h{i}" for i in range(8))
+    header(s, p, "ethash", """// Ethash-style hashimoto nonce search (ethminer analogue, PAPER.md:876-879), lean-register form.
+// Generated by kernels/gen_crypto.py (HF_ETHASH_FORM=lean). seed = Keccak-512(header_hash[8 words] ||
+// nonce as 64-bit LE); mix = seed repeated to 32 words; 64 rounds: page = fnv(i ^ seed[0],
+// mix[i % 32]) % npages (ethminer's modulo walk; remu: the fnv word read as uint32),
+// mix = fnv(mix, dag[page]) over the 128-byte page; cmix = 8-word fnv fold;
+// result = Keccak-256(seed || cmix).
+// B200 mechanics: every thread computes the two Keccaks of its own nonce and parks the seed in
+// shared memory; the DAG walk of the 8 nonces of an 8-lane group is shared (lane j holds words
+// 4j..4j+3 of the 8 mixes, the lane owning mix[i % 32] computes each page index and broadcasts
+// it with one shfl.idx) and every round's 8 pages per lane are copied by 16-byte cp.async into a
+// per-thread shared ring (8 x 16 B), so pages in flight cost no registers: the walk needs ~60
+// registers instead of ~125, and twice the warps (pages in flight) fit per SM.
+// Criterion/checksum word = result word 0 (little-endian). Any warp-multiple block size up to """ + str(T) + """
+// works (tunable: the partition search sizes it against its partner).""",
+           f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], int {p}_dag[], int {p}_rc[], {hp}, int {p}_npages, "
+           f"int {p}_nonce0, int {p}_count, int {p}_target", T, fixed=False)
+    s(f"shared int {p}_ring[{8 * T * 4}];")
+    s(f"shared int {p}_seed[{16 * S}];")
+    A = {(x, y): Lane(f"a{x}{y}l", f"a{x}{y}h") for x in range(5) for y in range(5)}
+    names = []
+    for x in range(5):
+        for y in range(5):
+            names += [f"a{x}{y}l", f"a{x}{y}h"]
+    for x in range(5):
+        names += [f"c{x}l", f"c{x}h"]
+    names += ["dl", "dh"] + [f"cm{i}" for i in range(8)]
+    names += [f"x{h}_{k}" for h in range(8) for k in range(4)] + [f"z{h}" for h in range(8)]
+    names += [f"pg{h}" for h in range(8)] + ["q0", "q1", "q2", "q3", "bw", "cw", "r0", "lj", "gb", "valid", "nonce"]
+    names += ["tl", "th", "ul", "uh"]
+    decls(s, names)
+    s("int tid = threadIdx.x;")
+    s("int nthr = blockDim.x;")
+    s("int best = 2147483647;")
+    s("int cnt = 0;")
+    s("int chk = 0;")
+    s("int lane = tid % 32;")
+    s("lj = lane % 8;")
+    s("gb = tid - lj;")
+    s(f"for (int n0 = blockIdx.x * nthr + (tid / 32) * 32; n0 < {p}_count; n0 = n0 + gridDim.x * nthr) {{")
+    s.ind += 1
+    s("valid = n0 + lane < " + f"{p}_count;")
+    s(f"nonce = {p}_nonce0 + n0 + lane;")
+    words = [f"{p}_h{i}" for i in range(8)] + ["nonce", "0", "0x00000001"] + ["0"] * 6 + ["0x80000000"]
+    absorb_words(s, A, words)
+    keccak_f(s, A, f"{p}_rc")
+    for i in range(8):
+        ln = A[(i % 5, i // 5)]
+        s(f"{p}_seed[{2 * i * S} + tid] = {ln.lo};")
+        s(f"{p}_seed[{(2 * i + 1) * S} + tid] = {ln.hi};")
+    s("warp_sync();")
+    # lane j of the group takes words 4(j % 4) .. 4(j % 4) + 3 of each of the 8 group seeds
+    s("int wrow = (lj % 4) * 4;")
+    for h in range(8):
+        s(f"z{h} = {p}_seed[gb + {h}];")
+        for k in range(4):
+            s(f"x{h}_{k} = {p}_seed[(wrow + {k}) * {S} + gb + {h}];")
+    s("for (int it = 0; it < 64; it = it + 4) {")
+    s.ind += 1
+    s("int owner = (it % 32) / 4;")
+    for k in range(4):
+        for h in range(8):
+            s(f"pg{h} = ((it + {k}) ^ z{h}) * 16777619 ^ x{h}_{k};")
+            bcast8(s, f"pg{h}", "owner")
+            s(f"pg{h} = remu(pg{h}, {p}_npages) * 8 + lj;")
+        for h in range(8):
+            s(f"async_copy({p}_ring, {h * T} + tid, {p}_dag, pg{h});")
+        s("async_wait();")
+        for h in range(8):
+            s(f"vload({p}_ring, {h * T} + tid, q0, q1, q2, q3);")
+            for j in range(4):
+                s(f"x{h}_{j} = x{h}_{j} * 16777619 ^ q{j};")
+    s.ind -= 1
+    s("}")
+    # cmix word j of nonce h sits in lane j of the group; each lane collects its own nonce's 8
+    for h in range(8):
+        s(f"cw = ((x{h}_0 * 16777619 ^ x{h}_1) * 16777619 ^ x{h}_2) * 16777619 ^ x{h}_3;")
+        for k in range(8):
+            s("bw = cw;")
+            bcast8(s, "bw", k)
+            s(f"if (lj == {h}) {{")
+            s(f"  cm{k} = bw;")
+            s("}")
+    words = [f"{p}_seed[{i * S} + tid]" for i in range(16)] + [f"cm{i}" for i in range(8)] + ["0x00000001"] + ["0"] * 8 + ["0x80000000"]
+    absorb_words(s, A, words)
+    s("warp_sync();")  # every lane read its seed before the next nonce batch overwrites it
+    keccak_f(s, A, f"{p}_rc")
+    s(f"r0 = {A[(0, 0)].lo};")
+    s("if (valid) {")
+    s("  chk = chk + r0;")
+    s(f"  if (ltu(r0, {p}_target)) {{")
+    s("    cnt = cnt + 1;")
+    s("    best = min(best, nonce);")
+    s("  }")
+    s("}")
+    s.ind -= 1
+    s("}")
+    s(f"atomic_add({p}_chk[0], chk);")
+    s("if (cnt > 0) {")
+    s(f"  atomic_add({p}_cnt[0], cnt);")
+    s("}")
+    tail(s, p)
+    return s.text()
+
+
+def gen_ethash_reg():
+    global ETHASH_FORM
+    form, ETHASH_FORM = ETHASH_FORM, "reg"
+    try:
+        return gen_ethash()
+    finally:
+        ETHASH_FORM = form
+
+
 def main():
     out = os.path.join(HERE, "b200")
     for name, gen in (("sha256d", gen_sha256d), ("blake256", gen_blake256), ("blake2b", gen_blake2b),
-                      ("ethash", gen_ethash)):
+                      ("ethash", gen_ethash), ("ethash_reg", gen_ethash_reg)):
         with open(os.path.join(out, name + ".mk"), "w") as f:
             f.write(gen())
         print("wrote", name)

@@ -35,7 +35,8 @@ def test_known_answer_vectors():
 def test_generated_sources_are_current(tmp_path):
     from paper_2007_01277_b200.kernels import gen_crypto
     for kind, gen in (("sha256d", gen_crypto.gen_sha256d), ("blake256", gen_crypto.gen_blake256),
-                      ("blake2b", gen_crypto.gen_blake2b), ("ethash", gen_crypto.gen_ethash)):
+                      ("blake2b", gen_crypto.gen_blake2b), ("ethash", gen_crypto.gen_ethash),
+                      ("ethash_reg", gen_crypto.gen_ethash_reg)):
         assert gen() == src(kind), kind
 
 
@@ -64,23 +65,28 @@ def test_ethash_modulo_walk_on_reference_interpreter(hf, tmp_path):
 
 
 @pytest.mark.gpu
-def test_ethash_modulo_walk_on_device(gpu):
+@pytest.mark.parametrize("form", crypto.FORMS["ethash"])
+def test_ethash_modulo_walk_on_device(gpu, form):
     hf = gpu
-    count, grid, nonce0, target = 512, 4, 99, 1 << 28
+    count, grid, nonce0, target = 2600, 4, 99, 1 << 28
     w = crypto.workload("ethash", count=count, grid=grid, nonce0=nonce0, target=target, npages=PRIME_PAGES)
     img = hf.Image(w.image).upload()
-    hf.Module.kernel(src("ethash"), grid=grid, specialize=img).run(img, grid)
+    hf.Module.kernel(src(form), grid=grid, specialize=img).run(img, grid)
     img.download()
-    assert device_outputs(img, "ethash") == reference_outputs("ethash", count, grid, nonce0, target,
+    thr = crypto.FORM_THREADS.get(form, crypto.THREADS["ethash"])
+    assert device_outputs(img, "ethash") == reference_outputs("ethash", count, grid, nonce0, target, threads=thr,
                                                               npages=PRIME_PAGES)
 
 
+FORMS = [(k, f) for k in KINDS for f in crypto.FORMS[k]]
+
+
 @pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
-@pytest.mark.parametrize("kind", KINDS)
-def test_lowered_kernels_on_reference_interpreter(hf, kind, tmp_path):
+@pytest.mark.parametrize("kind,form", FORMS)
+def test_lowered_kernels_on_reference_interpreter(hf, kind, form, tmp_path):
     count, grid, nonce0, target = (6 if kind == "ethash" else 40), 1, 1000, 1 << 31
     w = crypto.workload(kind, count=count, grid=grid, nonce0=nonce0, target=target)
-    (tmp_path / "k.mk").write_text(hf.lower(src(kind)))
+    (tmp_path / "k.mk").write_text(hf.lower(src(form)))
     (tmp_path / "k.img").write_text(w.image)
     _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img", "--grid", grid)
     arrays, _ = oracle.parse_image(dump)
@@ -98,15 +104,16 @@ def device_outputs(img, kind):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kind", KINDS)
-def test_crypto_member_on_device(gpu, kind):
+@pytest.mark.parametrize("kind,form", FORMS)
+def test_crypto_member_on_device(gpu, kind, form):
     hf = gpu
-    count, grid, nonce0, target = (512 if kind == "ethash" else 4096), 4, 77, 1 << 27
+    count, grid, nonce0, target = (2600 if kind == "ethash" else 4096), 4, 77, 1 << 27
     w = crypto.workload(kind, count=count, grid=grid, nonce0=nonce0, target=target)
     img = hf.Image(w.image).upload()
-    hf.Module.kernel(src(kind), grid=grid, specialize=img).run(img, grid)
+    hf.Module.kernel(src(form), grid=grid, specialize=img).run(img, grid)
     img.download()
-    assert device_outputs(img, kind) == reference_outputs(kind, count, grid, nonce0, target)
+    thr = crypto.FORM_THREADS.get(form, crypto.THREADS[kind])
+    assert device_outputs(img, kind) == reference_outputs(kind, count, grid, nonce0, target, threads=thr)
 
 
 @pytest.mark.gpu
@@ -132,11 +139,12 @@ def test_fused_crypto_pairs_on_device(gpu, a, b):
     wa = crypto.workload(a, count=ca, grid=grid, nonce0=5, target=1 << 28)
     wb = crypto.workload(b, count=cb, grid=grid, nonce0=9, target=1 << 28)
     img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
-    m = hf.Module.fused(src(a), src(b), crypto.THREADS[a], crypto.THREADS[b], grid=grid, specialize=img)
+    d2 = 512 if b == "ethash" else crypto.THREADS[b]  # the lean Ethash runs in any interval <= 1024
+    m = hf.Module.fused(src(a), src(b), crypto.THREADS[a], d2, grid=grid, specialize=img)
     m.run(img, grid)
     img.download()
     assert device_outputs(img, a) == reference_outputs(a, ca, grid, 5, 1 << 28)
-    assert device_outputs(img, b) == reference_outputs(b, cb, grid, 9, 1 << 28)
+    assert device_outputs(img, b) == reference_outputs(b, cb, grid, 9, 1 << 28, threads=d2)
 
 
 @pytest.mark.gpu
