@@ -69,7 +69,9 @@ configuration.
     ops = load("crypto_ops.json")
     c = replace_block(c, "**C3 — the paper's six crypto pairs**", "<!-- crypto-prose -->", f"""**C3 — the paper's six crypto pairs** (issue bound = source operations per nonce ×
 nonces / 32 / (148 SMs × 4 schedulers × f), `profiles/crypto_ops.json`; HBM bound = 8 KiB of
-DAG per Ethash nonce at the copy bandwidth; frac = the larger bound / fused time):
+DAG per Ethash nonce at the copy bandwidth / at the random-page ceiling the bench measures on the
+same DAG; frac = the larger of the issue and random-page bounds / fused time; every unfused baseline
+runs each member's fastest source form):
 
 {crypto.rstrip()}
 
@@ -82,21 +84,23 @@ DAG per Ethash nonce at the copy bandwidth; frac = the larger bound / fused time
     slots = 148 * 4 * line["clocks"]["sm_mhz"] * 1e6
 
     def cfrac(p):
-        a, b = p["pair"].split("+")
-        n = p["nonces"]
-        ti = sum(n[k] * ops[k]["ops_per_nonce"] / 32 for k in (a, b)) / slots * 1e6
-        return max(ti, n.get("ethash", 0) * 8192 / (6558.7 * 1e3)) / p["fused_us"]
+        return p["roofline"]["frac"]
     ef = [cfrac(p) for p in eth]
     c = replace_block(c, "<!-- crypto-prose -->", "**The ALU pipe is the crypto pairs' real ceiling.**", f"""<!-- crypto-prose -->
 {len(cwins)} of {len(cr)} pairs win, by {min(p['speedup'] for p in cwins) * 100 - 100:.1f}–{max(p['speedup'] for p in cwins) * 100 - 100:.1f} %, {nbud} of them with per-interval
 `setmaxnreg` budgets{'; below: ' + ', '.join(closs) + ' (two ALU-pipe-bound hashes)' if closs else ''}. All four hashes are tunable, so
 the search also sizes the hash interval (e.g. a 128-thread BLAKE-256 interval beside a 640-thread
-Ethash one). The Ethash pairs sit at {min(ef):.2f}–{max(ef):.2f} of their bound: Ethash alone reads its random
-128-B DAG pages at 4.4 TB/s (1,937 µs for 2^20 nonces) with 127 registers and 16 warps per SM, and a
-fused interval gets fewer (Ethash capped at 96 alone: 2,364 µs). nvdisasm's live-range dump puts
-the 122-register peak inside the Keccak round (theta) rather than in the DAG walk, and staging the
-DAG pages through shared memory with MK+ `async_copy` (no register holds a page in flight) changes
-Ethash alone by −2 % and the best fused pair by +1 % (`profiles/r02_probe_ethash_async.jsonl`).
+Ethash one). The Ethash pairs sit at {min(ef):.2f}–{max(ef):.2f} of their bound. Their fused member is the
+lean-register Ethash (`kernels/b200/ethash.mk`, §7): the DAG pages land in a per-thread shared
+ring through 16-byte `cp.async` copies and the Keccak-512 seed waits in shared memory across the
+walk, so the walk holds only the mixes — 64 registers at 1,024 threads against the register form's
+127 at 256 — and a fused Ethash interval keeps its warps: every Ethash pair fuses 5–13 % faster than
+with the register form (`profiles/r02_probe_ethash_lean.jsonl`). Alone the lean form is ~5 % slower
+than the register form (`ethash_reg.mk`: 2,000 vs 2,104 µs), so the unfused baselines run the register
+form. Ethash alone reads its DAG at 4.3 TB/s, 0.75 of the {det['crypto']['dag_ceiling']['gbs'] / 1e3:.2f} TB/s
+random-page ceiling measured on the same DAG (`kernels/probe/dag_pages.mk`,
+`profiles/r02_probe_random2.jsonl`: 4.5–5.7 TB/s across launch shapes, dependent or independent
+chains alike): random 128-B pages do not stream at the copy figure.
 
 """)
     summ = load("r02_ncu_summary.json")["pairs"]

@@ -18,6 +18,7 @@ ap.add_argument("--detail", default=os.path.join(ROOT, "profiles", "r02_bench_de
 ap.add_argument("--only", default="", help="comma list of pairs (default all)")
 ap.add_argument("--fused-only", action="store_true")
 ap.add_argument("--no-crypto", action="store_true")
+ap.add_argument("--no-dl", action="store_true")
 ap.add_argument("--finalists", action="store_true",
                 help="also launch every re-timed finalist configuration of the search (trace 'final' rows)")
 args = ap.parse_args()
@@ -31,7 +32,7 @@ def build(sa, sb, c, img):
 
 
 for r in d["results"]:
-    if only and r["pair"] not in only:
+    if args.no_dl or (only and r["pair"] not in only):
         continue
     a, b = r["pair"].split("+")
     img = hf.Image(P.MEMBERS[a].sizes["full"]().image).merge(hf.Image(P.MEMBERS[b].sizes["full"]().image)).upload()
@@ -60,8 +61,10 @@ if not args.no_crypto:
         img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
         sa = open(os.path.join(P.KERNELS, "b200", a + ".mk")).read()
         sb = open(os.path.join(P.KERNELS, "b200", b + ".mk")).read()
-        if not args.fused_only:
-            for k, s, g in ((a, sa, c["grid_a"]), (b, sb, c["grid_b"])):
+        if not args.fused_only:  # each member in the form its unfused baseline ran (bench baseline_forms)
+            forms = c.get("baseline_forms") or {}
+            for k, g in ((a, c["grid_a"]), (b, c["grid_b"])):
+                s = open(os.path.join(P.KERNELS, "b200", forms.get(k, k) + ".mk")).read()
                 hf.Module.kernel(s, grid=g, specialize=img).run(img, g)
                 order.append(f"{c['pair']}:{k}")
         build(sa, sb, c, img).run(img, c["grid"])

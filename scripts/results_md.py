@@ -32,22 +32,27 @@ if not d.get("crypto"):
     print("\n".join(o))
     sys.exit(0)
 o.append("")
-o.append("| crypto pair | partition | registers | fused µs | seq µs | 2-stream µs | speed-up | issue bound µs | HBM bound µs | roofline frac |")
-o.append("|---|---|---|---|---|---|---|---|---|---|")
-slots = 148 * 4 * line["clocks"]["sm_mhz"] * 1e6
+o.append("| crypto pair | partition | registers | baseline forms | fused µs | seq µs | 2-stream µs | speed-up | "
+         "issue bound µs | HBM bound µs (copy / random-page) | roofline frac |")
+o.append("|---|---|---|---|---|---|---|---|---|---|---|")
+dc = d["crypto"].get("dag_ceiling") or {}
 for c in d["crypto"]["pairs"]:
     if c["pair"] == "upsample+blake256":
         continue
-    a, b = c["pair"].split("+")
-    n = c["nonces"]
-    ti = sum(n[k] * ops[k]["ops_per_nonce"] / 32 for k in (a, b)) / slots * 1e6
-    th = n.get("ethash", 0) * 8192 / (hbm * 1e3)
+    rf = c["roofline"]
     regs = f"budgets {c['interval_regs'][0]}/{c['interval_regs'][1]}" if c.get("interval_regs") else \
         (f"cap {c['reg_cap']}" if c.get("reg_cap") else f"uncapped ({c['regs']})")
+    forms = "/".join(v for v in (c.get("baseline_forms") or {}).values()) or "—"
+    hb = "—" if not rf.get("hbm_us") else (f"{rf['hbm_us']:.0f} / {rf['hbm_random_us']:.0f}" if rf.get("hbm_random_us")
+                                          else f"{rf['hbm_us']:.0f}")
     sp = c["speedup"]
-    o.append(f"| {c['pair']} | {c['d1']}/{c['d2']} @ {c['grid']} | {regs} | {c['fused_us']:.0f} | {c['seq_us']:.0f} | "
-             f"{c['two_stream_us']:.0f} | {'**%.3f**' % sp if sp > 1 else '%.3f' % sp} | {ti:.0f} | {th:.0f} | "
-             f"{max(ti, th) / c['fused_us']:.3f} |")
+    o.append(f"| {c['pair']} | {c['d1']}/{c['d2']} @ {c['grid']} | {regs} | {forms} | {c['fused_us']:.0f} | "
+             f"{c['seq_us']:.0f} | {c['two_stream_us']:.0f} | {'**%.3f**' % sp if sp > 1 else '%.3f' % sp} | "
+             f"{rf['issue_us']:.0f} | {hb} | {rf['frac']:.3f} |")
+if dc:
+    o.append("")
+    o.append(f"Random-page DAG ceiling (measured in the bench, `{dc['kernel']}`): {dc['gbs']:.0f} GB/s "
+             f"({dc['bytes'] / 1e9:.1f} GB of independent random 128-B pages in {dc['us']:.0f} µs, grid {dc['grid']}).")
 c4 = next((c for c in d["crypto"]["pairs"] if c["pair"] == "upsample+blake256"), None)
 if c4:
     o.append("")
