@@ -663,7 +663,7 @@ def gen_ethash_lean():
     for x in range(5):
         names += [f"c{x}l", f"c{x}h"]
     names += ["dl", "dh"] + [f"cm{i}" for i in range(8)]
-    names += [f"x{h}_{k}" for h in range(8) for k in range(4)] + ["zl", "wl", "pgm"]
+    names += [f"x{h}_{k}" for h in range(8) for k in range(4)] + [f"z{h}" for h in range(8)]
     names += [f"pg{h}" for h in range(8)] + ["q0", "q1", "q2", "q3", "bw", "cw", "r0", "lj", "gb", "valid", "nonce"]
     names += ["tl", "th", "ul", "uh"]
     decls(s, names)
@@ -689,27 +689,18 @@ def gen_ethash_lean():
     s("warp_sync();")
     # lane j of the group takes words 4(j % 4) .. 4(j % 4) + 3 of each of the 8 group seeds
     s("int wrow = (lj % 4) * 4;")
-    s(f"zl = {p}_seed[tid];")  # word 0 of this lane's own seed: lane j computes nonce j's page indices
     for h in range(8):
+        s(f"z{h} = {p}_seed[gb + {h}];")
         for k in range(4):
             s(f"x{h}_{k} = {p}_seed[(wrow + {k}) * {S} + gb + {h}];")
     s("for (int it = 0; it < 64; it = it + 4) {")
     s.ind += 1
     s("int owner = (it % 32) / 4;")
     for k in range(4):
-        # transposed index step: lane j collects mix word (it + k) % 32 of nonce j from the owner
-        # lane (8 shuffles), computes that ONE page index, and the group broadcasts the 8 indices
-        # (8 shuffles): one fnv + remu per lane instead of eight (the ALU pipe is the fused pairs'
-        # bound; the shuffles are not on it)
         for h in range(8):
-            s(f"bw = warp_bcast(x{h}_{k}, owner, 8);")
-            s(f"if (lj == {h}) {{")
-            s("  wl = bw;")
-            s("}")
-        s(f"pgm = remu(((it + {k}) ^ zl) * 16777619 ^ wl, {p}_npages);")
-        for h in range(8):
-            s(f"pg{h} = warp_bcast(pgm, {h}, 8);")
-            s(f"pg{h} = pg{h} * 8 + lj;")
+            s(f"pg{h} = ((it + {k}) ^ z{h}) * 16777619 ^ x{h}_{k};")
+            bcast8(s, f"pg{h}", "owner")
+            s(f"pg{h} = remu(pg{h}, {p}_npages) * 8 + lj;")
         for h in range(8):
             s(f"async_copy({p}_ring, {h * T} + tid, {p}_dag, pg{h});")
         s("async_wait();")
