@@ -63,6 +63,8 @@ def workload(kind: str, count: int, grid: int, nonce0: int = 0, target: int = 1 
     lines += [f"scalar {p}_nonce0 int32 {i32(nonce0)}", f"scalar {p}_count int32 {count}",
               f"scalar {p}_target int32 {i32(target)}"]
     dag_bytes = 0
+    if kind == "sha256d":  # powers of two for the FMA-pipe rotates (gen_crypto HF_SHA_PIPES=fma, not the default)
+        lines.append(f"array {p}_pw int32 32 values " + " ".join(str(i32(1 << k)) for k in range(32)))
     if kind == "ethash":
         rc = []
         for r in KECCAK_RC:

@@ -894,6 +894,7 @@ class Parser {
           else if (b200() && n.text == "warp_bcast") w = Intr::Bcast;
           else if (b200() && n.text == "addc") w = Intr::Addc;
           else if (b200() && n.text == "remu") w = Intr::RemU;
+          else if (b200() && n.text == "mulhi_u") w = Intr::MulHiU;
           if (w) {
             std::vector<Expr> a = args();
             if (int(a.size()) != intr_arity(*w))

@@ -45,6 +45,7 @@ const char* intr_name(Intr i) {
     case Intr::Bcast: return "warp_bcast";
     case Intr::Addc: return "addc";
     case Intr::RemU: return "remu";
+    case Intr::MulHiU: return "mulhi_u";
   }
   return "?";
 }

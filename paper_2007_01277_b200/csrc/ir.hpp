@@ -76,6 +76,9 @@ enum class Intr : uint8_t {
             // device: add.cc + addc, i.e. IADD3 + IADD3.X instead of an unsigned compare)
   RemU,     // remu(a, b): a mod b with a read as uint32, for 0 < b < 2^30 (Ethash's page walk);
             // device: one unsigned remainder; plain MK: ((shr_u(a, 1) % b) * 2 + (a & 1)) % b
+  MulHiU,   // mulhi_u(a, b): high word of the unsigned 64-bit product a * b (device: IMAD.HI.U32 on
+            // the FMA pipe, e.g. x >> n as mulhi_u(x, 2^(32-n)) with the power in a register);
+            // plain MK: the 16-bit-limb schoolbook product
 };
 const char* intr_name(Intr i);
 int intr_arity(Intr i);

@@ -684,6 +684,18 @@ struct Lowerer {
         Expr half = binary(Bin::Mod, shr_u(x, lit(1)), n);
         return binary(Bin::Mod, binary(Bin::Add, binary(Bin::Mul, half, lit(2)), binary(Bin::And, x, lit(1))), n);
       }
+      case Intr::MulHiU: {
+        // 16-bit limbs: a = ah:al, b = bh:bl; every partial product and sum wraps mod 2^32 like
+        // the interpreter's int arithmetic, and only the bits each term contributes are kept
+        Expr al = binary(Bin::And, x, lit(0xffff)), ah = shr_u(x, lit(16));
+        Expr bl = binary(Bin::And, n, lit(0xffff)), bh = shr_u(n, lit(16));
+        Expr ll = binary(Bin::Mul, al, bl), lh = binary(Bin::Mul, al, bh);
+        Expr hl = binary(Bin::Mul, ah, bl), hh = binary(Bin::Mul, ah, bh);
+        Expr mid = binary(Bin::Add, binary(Bin::Add, shr_u(ll, lit(16)), binary(Bin::And, lh, lit(0xffff))),
+                          binary(Bin::And, hl, lit(0xffff)));
+        return binary(Bin::Add, binary(Bin::Add, binary(Bin::Add, hh, shr_u(lh, lit(16))), shr_u(hl, lit(16))),
+                      shr_u(mid, lit(16)));
+      }
       case Intr::Addc: {
         // ahi + bhi + ltu(alo + blo, alo), with ltu spelled out as above
         Expr lo = binary(Bin::Add, c.a[2], c.a[3]);

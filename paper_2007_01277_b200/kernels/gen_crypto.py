@@ -162,19 +162,54 @@ def loop_close(src, p, word, crit):
 # SHA-256d
 # ---------------------------------------------------------------------------------------
 
+# SHA-256 pipe balance (HF_SHA_PIPES): "alu" = every rotate/shift a funnel shift (SHF) and every
+# add an IADD3, all on the ALU pipe, which SHA-256d saturates (98 % busy, FMA pipe 5 %);
+# "fma" = two of the three rotates of each Sigma/sigma and the sigma shifts as multiplies by a
+# power of two held in a register (x << k = x * 2^k: IMAD; x >> (32 - k) = mulhi_u(x, 2^k):
+# IMAD.HI; the halves of a rotate have disjoint bits, so they join the Sigma's XOR directly),
+# which moves about a third of the round's work to the idle FMA pipe. The powers come from the
+# sh_pw array (a register the compiler cannot fold into a shift). Measured on B200: ptxas turns each
+# rotate half-pair into one IMAD.WIDE.U32, which is far slower than the SHF it replaces (SHA-256d
+# alone 2,846 vs 2,138 us, every fused pair 16-20 % slower; profiles/r02_probe_sha_pipes.jsonl), so
+# the member keeps "alu".
+SHA_PIPES = os.environ.get("HF_SHA_PIPES", "alu")
+SHA_POW = {26: "pw26", 21: "pw21", 30: "pw30", 19: "pw19", 25: "pw25", 14: "pw14", 15: "pw15", 13: "pw13",
+           29: "pw29", 22: "pw22"}
+
+
+def _rot_fma(x, n):
+    """rotr(x, n) as the XOR of its two disjoint halves, both on the FMA pipe."""
+    k = SHA_POW[32 - n]
+    return f"({x} * {k}) ^ mulhi_u({x}, {k})"
+
+
+def _shr_fma(x, n):
+    return f"mulhi_u({x}, {SHA_POW[32 - n]})"
+
+
 def sha_rounds(src, roles, w, first_w=None):
     """64 rounds; roles = list of 8 variable names (a..h); w = 16 schedule variable names.
     Returns the final roles."""
     R = list(roles)
+    fma = SHA_PIPES == "fma"
     for i in range(64):
         if i >= 16:
             x, x2, x7, x15 = w[i % 16], w[(i - 2) % 16], w[(i - 7) % 16], w[(i - 15) % 16]
-            src(f"{x} = (rotr({x2}, 17) ^ rotr({x2}, 19) ^ shr_u({x2}, 10)) + {x7} + "
-                f"(rotr({x15}, 7) ^ rotr({x15}, 18) ^ shr_u({x15}, 3)) + {x};")
+            if fma:
+                src(f"{x} = ({_rot_fma(x2, 17)} ^ {_rot_fma(x2, 19)} ^ {_shr_fma(x2, 10)}) + {x7} + "
+                    f"({_rot_fma(x15, 7)} ^ {_rot_fma(x15, 18)} ^ {_shr_fma(x15, 3)}) + {x};")
+            else:
+                src(f"{x} = (rotr({x2}, 17) ^ rotr({x2}, 19) ^ shr_u({x2}, 10)) + {x7} + "
+                    f"(rotr({x15}, 7) ^ rotr({x15}, 18) ^ shr_u({x15}, 3)) + {x};")
         a, b, c, d, e, f, g, h = R
-        src(f"t1 = {h} + (rotr({e}, 6) ^ rotr({e}, 11) ^ rotr({e}, 25)) + ({g} ^ ({e} & ({f} ^ {g}))) + "
-            f"{hx(SHA_K[i])} + {w[i % 16]};")
-        src(f"t2 = (rotr({a}, 2) ^ rotr({a}, 13) ^ rotr({a}, 22)) + (({a} & {b}) | ({c} & ({a} | {b})));")
+        if fma:
+            s1 = f"({_rot_fma(e, 6)} ^ {_rot_fma(e, 11)} ^ rotr({e}, 25))"
+            s0 = f"({_rot_fma(a, 2)} ^ {_rot_fma(a, 13)} ^ rotr({a}, 22))"
+        else:
+            s1 = f"(rotr({e}, 6) ^ rotr({e}, 11) ^ rotr({e}, 25))"
+            s0 = f"(rotr({a}, 2) ^ rotr({a}, 13) ^ rotr({a}, 22))"
+        src(f"t1 = {h} + {s1} + ({g} ^ ({e} & ({f} ^ {g}))) + {hx(SHA_K[i])} + {w[i % 16]};")
+        src(f"t2 = {s0} + (({a} & {b}) | ({c} & ({a} | {b})));")
         src(f"{d} = {d} + t1;")
         src(f"{h} = t1 + t2;")
         R = [h, a, b, c, d, e, f, g]
@@ -189,14 +224,17 @@ def gen_sha256d():
 // Generated by kernels/gen_crypto.py. Header = 20 big-endian words (scalar params h0..h18,
 // word 19 = bswap(nonce)); digest = SHA256(SHA256(header)); criterion word = digest[7].
 // The nonce-independent first block (the midstate) is compressed once per thread.""",
-           f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], {hp}, int {p}_nonce0, int {p}_count, int {p}_target",
-           512)
+           f"int {p}_cnt[], int {p}_chk[], int {p}_bmin[], {hp}, int {p}_nonce0, int {p}_count, int {p}_target"
+           + (f", int {p}_pw[]" if SHA_PIPES == "fma" else ""), 512)
     st = [f"s{c}" for c in "abcdefgh"]
     w = [f"w{i}" for i in range(16)]
     mid = [f"m{i}" for i in range(8)]
     dig = [f"d{i}" for i in range(8)]
     decls(s, st + w + mid + dig + ["t1", "t2"])
     loop_head(s, p)
+    if SHA_PIPES == "fma":
+        for k, v in sorted(SHA_POW.items()):
+            s(f"int {v} = {p}_pw[{k}];")
     for i in range(8):
         s(f"{st[i]} = {hx(IV256[i])};")
     for i in range(16):

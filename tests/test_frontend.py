@@ -224,6 +224,37 @@ def test_addc_is_the_high_word_of_a_64_bit_add(hf, tmp_path):
     assert "add.cc.u32" in hf.emit_kernel(ADDC)
 
 
+MULHI = """kernel k(int a[], int b[], int o[]) dims (256, 1, 1) {
+  int t = threadIdx.x;
+  o[t] = mulhi_u(a[t], b[t]);
+}
+"""
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_mulhi_u_is_the_high_word_of_an_unsigned_product(hf, tmp_path):
+    """MK+ mulhi_u(a, b): lowered (16-bit limbs) on the reference interpreter it equals the high
+    word of the unsigned 64-bit product, incl. 0, 1, -1 and powers of two (x >> n as
+    mulhi_u(x, 2^(32-n))); the sm_100a emission is __umulhi."""
+    import numpy as np
+    special = [0, 1, -1, -2147483648, 2147483647, 65535, 65536, -65536, 1 << 16, 1 << 26, 1 << 31 - 1]
+    img = ("array a int32 256 seed 5 range -2147483648 2147483647\n"
+           "array b int32 256 values " + " ".join(str(v) for v in special) + " " +
+           " ".join(str(((i * 2654435761) & 0xFFFFFFFF) - (1 << 32) if ((i * 2654435761) & 0xFFFFFFFF) >= 1 << 31
+                        else (i * 2654435761) & 0xFFFFFFFF) for i in range(256 - len(special))) +
+           "\narray o int32 256 zero\n")
+    (tmp_path / "k.mk").write_text(hf.lower(MULHI))
+    (tmp_path / "k.img").write_text(img)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img")
+    out, _ = oracle.parse_image(dump)
+    x, _ = oracle.parse_image(img)
+    ua = np.asarray(x["a"], np.int64).astype(np.uint64) & np.uint64(0xFFFFFFFF)
+    ub = np.asarray(x["b"], np.int64).astype(np.uint64) & np.uint64(0xFFFFFFFF)
+    want = ((ua * ub) >> np.uint64(32)).astype(np.int64)
+    assert np.array_equal(np.asarray(out["o"], np.int64) & 0xFFFFFFFF, want)
+    assert "__umulhi(" in hf.emit_kernel(MULHI)
+
+
 def test_vstore_cs_is_a_streaming_vstore(hf):
     """vstore_cs: same semantics as vstore (the lowering is identical), printed back as written,
     kept through fusion, emitted as an evict-first __stcs store on sm_100a."""
