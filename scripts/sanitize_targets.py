@@ -40,6 +40,13 @@ for a, b, d2, regs in [("sha256d", "blake2b", 512, (40, 56)), ("blake256", "etha
     hf.Module.fused(src[a], src[b], 512, d2, grid=2, specialize=img).run(img, 2)
     hf.Module.fused_regs(src[a], src[b], 512, d2, *regs, grid=2, specialize=img).run(img, 2)
     n += 2
+# Ethash alone in both forms (the lean member parks seeds in shared memory across warp_sync and
+# stages DAG pages through cp.async; 1,024 threads at 2 blocks)
+we = CR.workload("ethash", 2600, 2, nonce0=3, target=1 << 28)
+img = hf.Image(we.image).upload()
+for form in CR.FORMS["ethash"]:
+    hf.Module.kernel(open(os.path.join(P.KERNELS, "b200", form + ".mk")).read(), grid=2, specialize=img).run(img, 2)
+    n += 1
 img = hf.Image(P._bn(2, 8, 56 * 56, slots=256)(0).image).upload()
 hf.Module.kernel(P.source("b200", "batchnorm_warp"), grid=7).run(img, 7)
 n += 1
