@@ -42,7 +42,7 @@ for a, b, d2, regs in [("sha256d", "blake2b", 512, (40, 56)), ("blake256", "etha
     n += 2
 # Ethash alone in both forms (the lean member parks seeds in shared memory across warp_sync and
 # stages DAG pages through cp.async; 1,024 threads at 2 blocks)
-we = CR.workload("ethash", 2600, 2, nonce0=3, target=1 << 28)
+we = CR.workload("ethash", 64, 2, nonce0=3, target=1 << 28)  # racecheck instruments every shared access: keep it small
 img = hf.Image(we.image).upload()
 for form in CR.FORMS["ethash"]:
     hf.Module.kernel(open(os.path.join(P.KERNELS, "b200", form + ".mk")).read(), grid=2, specialize=img).run(img, 2)
