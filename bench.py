@@ -738,19 +738,33 @@ def main():
     if world == 1 and args.ratios != "none":
         ratio_res = ratio_study(hf, P, pair_list, src, shape, grids, d0s, stream, args)
 
-    traffic = None
+    traffic, traffic_cfg = None, None
     tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tpath):
         try:
-            # ncu dram__bytes_read.sum + dram__bytes_write.sum of this fused kernel, one launch
+            # ncu dram__bytes_read.sum + dram__bytes_write.sum of this fused kernel, one launch:
+            # at the benched configuration when ncu measured it, else the measured configuration of
+            # the same pair and size nearest to it (the search can land on a neighbour run to run;
+            # the DRAM bytes of a pair barely move with the split), named in traffic_config
             entries = json.load(open(tpath)).get(f"{da}+{db}") or []
             if isinstance(entries, dict):
                 entries = [entries]
-            for t in entries:  # measured at the benched configuration and size, if ncu saw it
-                if t.get("config") == cfgs[dom_i] and t.get("algorithmic_bytes") == dom_bytes:
-                    traffic = t["dram_bytes"]
+            same = [t for t in entries if t.get("algorithmic_bytes") == dom_bytes]
+            exact = [t for t in same if t.get("config") == cfgs[dom_i]]
+
+            def dist(t):
+                c, r = t.get("config") or {}, cfgs[dom_i]
+                return (sum(c.get(k) != r.get(k) for k in ("d1", "d2", "grid", "split_grid", "reg_cap")),
+                        abs((c.get("d1") or 0) - (r.get("d1") or 0)))
+            pick = exact[0] if exact else (min(same, key=dist) if same else None)
+            if pick is not None:
+                traffic = pick["dram_bytes"]
+                c = pick.get("config") or {}
+                traffic_cfg = None if exact else (f"{c.get('d1')}/{c.get('d2')}@{c.get('grid')}"
+                                                  + (f" split {c['split_grid']}" if c.get("split_grid") else "")
+                                                  + (f" cap {c['reg_cap']}" if c.get("reg_cap") else ""))
         except Exception:
-            traffic = None
+            traffic, traffic_cfg = None, None
 
     if rank != 0:
         D.close()
@@ -803,7 +817,8 @@ def main():
                   for r in results},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "kernel": f"fused {da}+{db}",
-                     "algorithmic_bytes": dom_bytes, "peak_source": peak_src},
+                     "algorithmic_bytes": dom_bytes, "peak_source": peak_src,
+                     **({"traffic_config": traffic_cfg} if traffic_cfg else {})},
         "e2e": {"value": round(e2e["value"], 1), "unit": "us", "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
                 "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]},
         "gpu_launches": len(pair_list) * args.steps,
@@ -822,6 +837,9 @@ def main():
         line["crypto_parity"] = crypto_res["parity_ok"]
     text = json.dumps(line, separators=(",", ":"), ensure_ascii=False)
     for drop in ("unfused_step_us", "crypto_parity"):  # keep the headline parseable
+        if len(text.encode()) > LINE_LIMIT:
+            line["roofline"].pop("traffic_config", None)
+            text = json.dumps(line, separators=(",", ":"), ensure_ascii=False)
         if len(text.encode()) <= LINE_LIMIT:
             break
         line.pop(drop, None)
