@@ -895,6 +895,7 @@ class Parser {
           else if (b200() && n.text == "addc") w = Intr::Addc;
           else if (b200() && n.text == "remu") w = Intr::RemU;
           else if (b200() && n.text == "mulhi_u") w = Intr::MulHiU;
+          else if (b200() && n.text == "fma_add") w = Intr::FmaAdd;
           if (w) {
             std::vector<Expr> a = args();
             if (int(a.size()) != intr_arity(*w))

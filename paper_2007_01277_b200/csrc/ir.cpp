@@ -46,6 +46,7 @@ const char* intr_name(Intr i) {
     case Intr::Addc: return "addc";
     case Intr::RemU: return "remu";
     case Intr::MulHiU: return "mulhi_u";
+    case Intr::FmaAdd: return "fma_add";
   }
   return "?";
 }

@@ -79,6 +79,9 @@ enum class Intr : uint8_t {
   MulHiU,   // mulhi_u(a, b): high word of the unsigned 64-bit product a * b (device: IMAD.HI.U32 on
             // the FMA pipe, e.g. x >> n as mulhi_u(x, 2^(32-n)) with the power in a register);
             // plain MK: the 16-bit-limb schoolbook product
+  FmaAdd,   // fma_add(a, b): a + b (wrapping) issued on the FMA pipe (device: IMAD a, one, b with
+            // `one` a __constant__ the compiler cannot fold), so ALU-pipe-bound hash rounds can
+            // move adds off the saturated ALU pipe; plain MK: a + b
 };
 const char* intr_name(Intr i);
 int intr_arity(Intr i);

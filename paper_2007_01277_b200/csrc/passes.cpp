@@ -696,6 +696,8 @@ struct Lowerer {
         return binary(Bin::Add, binary(Bin::Add, binary(Bin::Add, hh, shr_u(lh, lit(16))), shr_u(hl, lit(16))),
                       shr_u(mid, lit(16)));
       }
+      case Intr::FmaAdd:
+        return binary(Bin::Add, x, n);
       case Intr::Addc: {
         // ahi + bhi + ltu(alo + blo, alo), with ltu spelled out as above
         Expr lo = binary(Bin::Add, c.a[2], c.a[3]);

@@ -187,11 +187,27 @@ def _shr_fma(x, n):
     return f"mulhi_u({x}, {SHA_POW[32 - n]})"
 
 
+# SHA-256 adds (HF_SHA_ADDS): "fma" writes every add of the round and the schedule as MK+
+# fma_add (IMAD a, one, b on the FMA pipe), leaving the ALU pipe the rotates and LOP3s only.
+SHA_ADDS = os.environ.get("HF_SHA_ADDS", "")
+
+
+def _sum(terms, fma):
+    """terms[0] + terms[1] + ...; with fma a left-to-right fma_add chain."""
+    if not fma:
+        return " + ".join(terms)
+    acc = terms[0]
+    for t in terms[1:]:
+        acc = f"fma_add({acc}, {t})"
+    return acc
+
+
 def sha_rounds(src, roles, w, first_w=None):
     """64 rounds; roles = list of 8 variable names (a..h); w = 16 schedule variable names.
     Returns the final roles."""
     R = list(roles)
     fma = SHA_PIPES == "fma"
+    fa = SHA_ADDS == "fma"
     for i in range(64):
         if i >= 16:
             x, x2, x7, x15 = w[i % 16], w[(i - 2) % 16], w[(i - 7) % 16], w[(i - 15) % 16]
@@ -199,8 +215,8 @@ def sha_rounds(src, roles, w, first_w=None):
                 src(f"{x} = ({_rot_fma(x2, 17)} ^ {_rot_fma(x2, 19)} ^ {_shr_fma(x2, 10)}) + {x7} + "
                     f"({_rot_fma(x15, 7)} ^ {_rot_fma(x15, 18)} ^ {_shr_fma(x15, 3)}) + {x};")
             else:
-                src(f"{x} = (rotr({x2}, 17) ^ rotr({x2}, 19) ^ shr_u({x2}, 10)) + {x7} + "
-                    f"(rotr({x15}, 7) ^ rotr({x15}, 18) ^ shr_u({x15}, 3)) + {x};")
+                src(f"{x} = " + _sum([f"(rotr({x2}, 17) ^ rotr({x2}, 19) ^ shr_u({x2}, 10))", x7,
+                                      f"(rotr({x15}, 7) ^ rotr({x15}, 18) ^ shr_u({x15}, 3))", x], fa) + ";")
         a, b, c, d, e, f, g, h = R
         if fma:
             s1 = f"({_rot_fma(e, 6)} ^ {_rot_fma(e, 11)} ^ rotr({e}, 25))"
@@ -208,10 +224,10 @@ def sha_rounds(src, roles, w, first_w=None):
         else:
             s1 = f"(rotr({e}, 6) ^ rotr({e}, 11) ^ rotr({e}, 25))"
             s0 = f"(rotr({a}, 2) ^ rotr({a}, 13) ^ rotr({a}, 22))"
-        src(f"t1 = {h} + {s1} + ({g} ^ ({e} & ({f} ^ {g}))) + {hx(SHA_K[i])} + {w[i % 16]};")
-        src(f"t2 = {s0} + (({a} & {b}) | ({c} & ({a} | {b})));")
-        src(f"{d} = {d} + t1;")
-        src(f"{h} = t1 + t2;")
+        src("t1 = " + _sum([h, s1, f"({g} ^ ({e} & ({f} ^ {g})))", hx(SHA_K[i]), w[i % 16]], fa) + ";")
+        src("t2 = " + _sum([s0, f"(({a} & {b}) | ({c} & ({a} | {b})))"], fa) + ";")
+        src(f"{d} = " + _sum([d, "t1"], fa) + ";")
+        src(f"{h} = " + _sum(["t1", "t2"], fa) + ";")
         R = [h, a, b, c, d, e, f, g]
     return R
 
@@ -278,8 +294,20 @@ def gen_sha256d():
 # BLAKE-256 (14 rounds)
 # ---------------------------------------------------------------------------------------
 
+# BLAKE-256 pipe balance (HF_B256_ADDS): the G function's adds are the only work of the round
+# that can leave the ALU pipe (XORs and rotates are LOP3/SHF, ALU-only); each letter moves one
+# add site onto the FMA pipe as MK+ fma_add (IMAD a, one, b): "a" = a = a + b + (m ^ c) (two
+# IMADs), "c" = c = c + d (one IMAD). "" keeps every add an IADD3 on the ALU pipe.
+B256_ADDS = os.environ.get("HF_B256_ADDS", "")
+
+
+def _add(x, y, fma):
+    return f"fma_add({x}, {y})" if fma else f"{x} + {y}"
+
+
 def blake256_compress(src, h, m, t, v):
     """m: 16 expressions (variable names or hex literals); t: counter (python int)."""
+    fa, fc = "a" in B256_ADDS, "c" in B256_ADDS
     for i in range(8):
         src(f"{v[i]} = {h[i]};")
     for i in range(4):
@@ -293,13 +321,13 @@ def blake256_compress(src, h, m, t, v):
         for i, (a, b, c, d) in enumerate(G_IDX):
             x, y = sg[2 * i], sg[2 * i + 1]
             A, B, Cc, D = v[a], v[b], v[c], v[d]
-            src(f"{A} = {A} + {B} + ({m[x]} ^ {hx(B256_C[y])});")
+            src(f"{A} = {_add(_add(A, B, fa), f'({m[x]} ^ {hx(B256_C[y])})', fa)};")
             src(f"{D} = rotr({D} ^ {A}, 16);")
-            src(f"{Cc} = {Cc} + {D};")
+            src(f"{Cc} = {_add(Cc, D, fc)};")
             src(f"{B} = rotr({B} ^ {Cc}, 12);")
-            src(f"{A} = {A} + {B} + ({m[y]} ^ {hx(B256_C[x])});")
+            src(f"{A} = {_add(_add(A, B, fa), f'({m[y]} ^ {hx(B256_C[x])})', fa)};")
             src(f"{D} = rotr({D} ^ {A}, 8);")
-            src(f"{Cc} = {Cc} + {D};")
+            src(f"{Cc} = {_add(Cc, D, fc)};")
             src(f"{B} = rotr({B} ^ {Cc}, 7);")
 
 

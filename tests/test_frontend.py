@@ -255,6 +255,37 @@ def test_mulhi_u_is_the_high_word_of_an_unsigned_product(hf, tmp_path):
     assert "__umulhi(" in hf.emit_kernel(MULHI)
 
 
+FMAADD = """kernel k(int a[], int b[], int o[]) dims (256, 1, 1) {
+  int t = threadIdx.x;
+  o[t] = fma_add(fma_add(a[t], b[t]), 7);
+}
+"""
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+def test_fma_add_is_a_wrapping_add(hf, tmp_path):
+    """MK+ fma_add(a, b): lowered to a plain + it wraps like the interpreter's int add (checked on
+    the reference interpreter at the int32 extremes); the sm_100a emission is a mad.lo.u32 with the
+    constant-memory one, so ptxas issues it on the FMA pipe (IMAD) instead of an IADD3."""
+    import numpy as np
+    special = [0, 1, -1, -2147483648, 2147483647, 2147483641, -7, 65536]
+    img = ("array a int32 256 seed 9 range -2147483648 2147483647\n"
+           "array b int32 256 values " + " ".join(str(v) for v in special) + " " +
+           " ".join(str((i * 7919) % 100003 - 50000) for i in range(256 - len(special))) +
+           "\narray o int32 256 zero\n")
+    low = hf.lower(FMAADD)
+    assert "fma_add" not in low
+    (tmp_path / "k.mk").write_text(low)
+    (tmp_path / "k.img").write_text(img)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img")
+    out, _ = oracle.parse_image(dump)
+    x, _ = oracle.parse_image(img)
+    want = (np.asarray(x["a"], np.int64) + np.asarray(x["b"], np.int64) + 7) & 0xFFFFFFFF
+    assert np.array_equal(np.asarray(out["o"], np.int64) & 0xFFFFFFFF, want)
+    src = hf.emit_kernel(FMAADD)
+    assert "hf_fma_add(hf_fma_add(" in src and "mad.lo.u32" in src and "__constant__ unsigned hf_one" in src
+
+
 def test_vstore_cs_is_a_streaming_vstore(hf):
     """vstore_cs: same semantics as vstore (the lowering is identical), printed back as written,
     kept through fusion, emitted as an evict-first __stcs store on sm_100a."""
