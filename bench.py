@@ -30,6 +30,7 @@ The last stdout line is a compact (<= 2 KB) JSON object; the search traces, per-
 crypto/C4 sweeps and parity details go to --detail (default profiles/r02_bench_detail.json).
 """
 import argparse
+import itertools
 import json
 import math
 import os
@@ -1020,25 +1021,27 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
                     del k
                 mg[name], base[name] = best_alone[1], best_alone[2]
             best, traces = None, []
-            for g in cgrids:
-                for d0 in ((1024,) if b != "ethash" else (768, 896, 1024)):
-                    try:
-                        r = hf.search(srcs[a], srcs[b], img, d0=d0, grid=g, reps=2, warmup=1, specialize=True,
-                                      flush_l2=False, extra_caps=(64, 96, 128) if b == "ethash" else (),
-                                      interval_regs=True)
-                    except hf.HFuseError:
-                        continue
-                    traces += [(g, x["d1"], x["d2"], x["reg_cap"], round(x["us"], 1)) for x in r["trace"]]
+            # every fused form pair (BLAKE2b: ltu and addc carries) over the grids and d0s
+            for fa, fb in itertools.product(CR.FUSED_FORMS[a], CR.FUSED_FORMS[b]):
+                for g in cgrids:
+                    for d0 in ((1024,) if b != "ethash" else (768, 896, 1024)):
+                        try:
+                            r = hf.search(forms[a][fa], forms[b][fb], img, d0=d0, grid=g, reps=2, warmup=1,
+                                          specialize=True, flush_l2=False,
+                                          extra_caps=(64, 96, 128) if b == "ethash" else (), interval_regs=True)
+                        except hf.HFuseError:
+                            continue
+                        traces += [(g, x["d1"], x["d2"], x["reg_cap"], round(x["us"], 1), fa, fb) for x in r["trace"]]
             # the three fastest screened points re-timed with a longer graph (a 2-repetition
             # screen of 3-ms kernels picks noise, like the DL search's short screens)
-            for g, d1, d2, cap, _ in sorted(traces, key=lambda t: t[4])[:3]:
-                cfg = {"d1": d1, "d2": d2, "grid": g, "reg_cap": None, "interval_regs": None}
+            for g, d1, d2, cap, _, fa, fb in sorted(traces, key=lambda t: t[4])[:3]:
+                cfg = {"d1": d1, "d2": d2, "grid": g, "reg_cap": None, "interval_regs": None, "forms": [fa, fb]}
                 if "/" in str(cap):
                     cfg["interval_regs"] = [int(x) for x in str(cap).split("/")]
                 elif cap not in ("none", None):
                     cfg["reg_cap"] = int(cap)
                 try:
-                    mm = build_fused(hf, srcs[a], srcs[b], cfg, img)
+                    mm = build_fused(hf, forms[a][fa], forms[b][fb], cfg, img)
                 except hf.HFuseError:
                     continue
                 t = gtime(hf, "single", mm, None, img, g, 0, stream, 3, 5)["mean_us"]
@@ -1048,7 +1051,8 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
             plan = {"mg": mg, "base": base, "cfg": best[0], "trace": traces}
         plan = D.bcast(plan)
         cfg, mg = plan["cfg"], plan["mg"]
-        m = build_fused(hf, srcs[a], srcs[b], cfg, img)
+        sa, sb = forms[a][cfg["forms"][0]], forms[b][cfg["forms"][1]]
+        m = build_fused(hf, sa, sb, cfg, img)
         res = {"pair": f"{a}+{b}", **cfg, "regs": m.info.regs, "nonces": {a: CRYPTO_COUNTS[a], b: CRYPTO_COUNTS[b]},
                "per_rank_nonces": {a: na, b: nb}}
         if rank == 0:
@@ -1087,7 +1091,7 @@ def crypto_suite(hf, torch, args, D, stream, sm_mhz=None, hbm_peak=6557.4):
         red = SH.reduce_gathered(layout, D.gather(packed) if world > 1 else packed.view(1, -1), None)["c"]
         res["hits"], res["winning_nonce"] = red[0].tolist(), red[1].tolist()
         if rank == 0 and not args.no_parity:
-            res["parity_ok"] = crypto_parity(hf, CR, srcs[a], srcs[b], a, b, cfg, cfg["d2"])
+            res["parity_ok"] = crypto_parity(hf, CR, sa, sb, a, b, cfg, cfg["d2"])
             out["parity_ok"] &= res["parity_ok"]
         out["pairs"].append(res)
         del m, img

@@ -9,8 +9,14 @@ from typing import List, Optional
 MEMBERS = {"sha256d": "sh", "blake256": "bl", "blake2b": "b2", "ethash": "eh"}
 THREADS = {"sha256d": 512, "blake256": 512, "blake2b": 512, "ethash": 1024}
 # member source files per kind: ethash.mk is the lean-register form (the fused member),
-# ethash_reg.mk the register form (faster alone; the bench's unfused baselines may run it)
-FORMS = {"sha256d": ["sha256d"], "blake256": ["blake256"], "blake2b": ["blake2b"], "ethash": ["ethash", "ethash_reg"]}
+# ethash_reg.mk the register form (faster alone); blake2b.mk carries its 64-bit adds with ltu
+# (compare + select: the select runs on the FMA pipe), blake2b_addc.mk with add.cc/addc (faster
+# alone, all ALU). The bench's unfused baselines run each kind's fastest form alone; the fused
+# search tries every form in FUSED_FORMS.
+FORMS = {"sha256d": ["sha256d"], "blake256": ["blake256"], "blake2b": ["blake2b", "blake2b_addc"],
+         "ethash": ["ethash", "ethash_reg"]}
+FUSED_FORMS = {"sha256d": ["sha256d"], "blake256": ["blake256"], "blake2b": ["blake2b", "blake2b_addc"],
+               "ethash": ["ethash"]}
 FORM_THREADS = {"ethash_reg": 256}
 # Genesis block header (Bitcoin), the SHA-256d known-answer vector, as 20 big-endian words.
 GENESIS_HEADER = bytes.fromhex(

@@ -59,8 +59,9 @@ if not args.no_crypto:
         wb = CR.workload(b, c["per_rank_nonces"][b], max(c["grid"], c["grid_a"], c["grid_b"]), target=1 << 12,
                          npages=33554393)
         img = hf.Image(wa.image).merge(hf.Image(wb.image)).upload()
-        sa = open(os.path.join(P.KERNELS, "b200", a + ".mk")).read()
-        sb = open(os.path.join(P.KERNELS, "b200", b + ".mk")).read()
+        fa, fb = c.get("forms") or (a, b)  # the member forms the bench fused
+        sa = open(os.path.join(P.KERNELS, "b200", fa + ".mk")).read()
+        sb = open(os.path.join(P.KERNELS, "b200", fb + ".mk")).read()
         if not args.fused_only:  # each member in the form its unfused baseline ran (bench baseline_forms)
             forms = c.get("baseline_forms") or {}
             for k, g in ((a, c["grid_a"]), (b, c["grid_b"])):

@@ -73,8 +73,9 @@ def main():
         wa = CR.workload(a, 1 << 20, c["grid"], target=1 << 12)
         wb = CR.workload(b, 1 << 20, c["grid"], target=1 << 12, npages=33554393)
         img = hf.Image(wa.image).merge(hf.Image(wb.image))
-        sa = open(os.path.join(P.KERNELS, "b200", a + ".mk")).read()
-        sb = open(os.path.join(P.KERNELS, "b200", b + ".mk")).read()
+        fa, fb = c.get("forms") or (a, b)  # the member forms the bench fused
+        sa = open(os.path.join(P.KERNELS, "b200", fa + ".mk")).read()
+        sb = open(os.path.join(P.KERNELS, "b200", fb + ".mk")).read()
         if c.get("interval_regs"):
             m = hf.Module.fused_regs(sa, sb, c["d1"], c["d2"], *c["interval_regs"], grid=c["grid"], specialize=img)
         else:

@@ -35,8 +35,8 @@ def test_known_answer_vectors():
 def test_generated_sources_are_current(tmp_path):
     from paper_2007_01277_b200.kernels import gen_crypto
     for kind, gen in (("sha256d", gen_crypto.gen_sha256d), ("blake256", gen_crypto.gen_blake256),
-                      ("blake2b", gen_crypto.gen_blake2b), ("ethash", gen_crypto.gen_ethash),
-                      ("ethash_reg", gen_crypto.gen_ethash_reg)):
+                      ("blake2b", gen_crypto.gen_blake2b), ("blake2b_addc", gen_crypto.gen_blake2b_addc),
+                      ("ethash", gen_crypto.gen_ethash), ("ethash_reg", gen_crypto.gen_ethash_reg)):
         assert gen() == src(kind), kind
 
 
