@@ -656,10 +656,19 @@ def main():
         if dist_on:
             reduce_step()
 
+    # Host-side launch cost must not leak into the device timings: at 1/8 shard sizes a kernel runs
+    # 7-10 us, about what one eager launch + two events cost on the host. So each timed region is
+    # queued behind a device-side spin (outside the region, after the synchronize + barrier) long
+    # enough for the host to enqueue all K steps; the GPU then runs them back to back and the
+    # events measure device time only.
+    spin_cycles = int(min(50e3, max(2e3, 30.0 * 2 * len(pair_list) * args.steps)) * 1e-6 * 2.0e9)
+
     def timed(fn):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         D.barrier()
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(spin_cycles)
         e0.record(stream)
         for s in range(args.steps):
             fn(s)

@@ -17,6 +17,16 @@ from paper_2007_01277_b200 import hfuse as hf  # noqa: E402
 from paper_2007_01277_b200 import pairs as P  # noqa: E402
 
 n = 0
+if sys.argv[1:] == ["ethash"]:  # the Ethash forms alone (their 1,024-thread / 192 KB launches)
+    we = CR.workload("ethash", 64, 2, nonce0=3, target=1 << 28)
+    img = hf.Image(we.image).upload()
+    for form in CR.FORMS["ethash"]:
+        m = hf.Module.kernel(open(os.path.join(P.KERNELS, "b200", form + ".mk")).read(), grid=2, specialize=img)
+        print(form, m.entry, "regs", m.info.regs, flush=True)
+        m.run(img, 2)
+        n += 1
+    print(f"sanitize targets: {n} fused launches")
+    sys.exit(0)
 corpus = golden("corpus_sources.json")
 digests = golden("corpus_digests.json")
 for a, b in [("histogram", "batchnorm"), ("batchnorm", "shuffle_reduce"), ("streamer", "hasher"),
