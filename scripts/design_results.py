@@ -206,6 +206,21 @@ exceed the HBM figure) and the line's `roofline` ({dom8['kernel']}, {dom8['algor
 the "%roofline at 1/8 B200" the metric asks for and why the shard step scales sub-linearly.
 
 """)
+    cp = [p for p in (det.get("crypto") or {}).get("pairs", []) if p["pair"] != "upsample+blake256"]
+    c4 = [p for p in (det.get("crypto") or {}).get("pairs", []) if p["pair"] == "upsample+blake256"]
+    cw = [p for p in cp if p["speedup"] >= 1.0]
+    cl = ", ".join(f"{p['pair']} {p['speedup']:.3f}" for p in cp if p["speedup"] < 1.0)
+    dl_lo = min(sp.values())
+    c = replace_block(c, "**North-star criterion (N1), honestly:**", "## 2.", f"""**North-star criterion (N1), honestly:** the best fused kernel is at or above the faster of
+sequential and two-stream launch on {wins} of 10 DL pairs at C2 sizes (lowest {dl_lo:.3f}, geomean
+{line['speedup_geomean']:.3f}), on {w3} of 10 at ResNet-50 conv3_x shapes, on {len(cw)} of {len(cp)} crypto pairs
+(below: {cl or 'none'}: two ALU-pipe-bound hashes, which two-stream launch already overlaps
+perfectly; every unfused baseline runs each member's fastest form){f" and on Upsample + BLAKE-256 ({c4[0]['speedup']:.2f})" if c4 else ""};
+the paper reports BN + Im2Col negative (`/root/reference/PAPER.md:1055-1057`). ncu issue-slot
+utilisation of the fused kernel is above its members' time-weighted combination
+(`combined_utilization`) in {ncomb} of {len(issue)} pairs and above both members in {nboth} (§10).
+
+""")
     c = re.sub(r"\(`combined_utilization`\) in \d+ of \d+ pairs and above both members in \d+ \(§10\)",
                f"(`combined_utilization`) in {ncomb} of {len(issue)} pairs and above both members in {nboth} (§10)", c)
     open(path, "w").write(c)

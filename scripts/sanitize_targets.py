@@ -54,7 +54,7 @@ for a, b, d2, regs in [("sha256d", "blake2b", 512, (40, 56)), ("blake256", "etha
 # stages DAG pages through cp.async; 1,024 threads at 2 blocks)
 we = CR.workload("ethash", 64, 2, nonce0=3, target=1 << 28)  # racecheck instruments every shared access: keep it small
 img = hf.Image(we.image).upload()
-for form in CR.FORMS["ethash"]:
+for form in ([] if sys.argv[1:] == ["no-ethash"] else CR.FORMS["ethash"]):
     hf.Module.kernel(open(os.path.join(P.KERNELS, "b200", form + ".mk")).read(), grid=2, specialize=img).run(img, 2)
     n += 1
 img = hf.Image(P._bn(2, 8, 56 * 56, slots=256)(0).image).upload()
