@@ -17,11 +17,17 @@ from paper_2007_01277_b200 import hfuse as hf  # noqa: E402
 from paper_2007_01277_b200 import pairs as P  # noqa: E402
 
 n = 0
-if sys.argv[1:] == ["ethash"]:  # the Ethash forms alone (their 1,024-thread / 192 KB launches)
-    we = CR.workload("ethash", 64, 2, nonce0=3, target=1 << 28)
+if sys.argv[1:2] == ["ethash"]:  # the Ethash forms alone (their 1,024-thread / 192 KB launches)
+    # optional: block size of the lean form (tunable) and nonce count
+    block = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    count = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
+    we = CR.workload("ethash", count, 2, nonce0=3, target=1 << 28)
     img = hf.Image(we.image).upload()
     for form in CR.FORMS["ethash"]:
-        m = hf.Module.kernel(open(os.path.join(P.KERNELS, "b200", form + ".mk")).read(), grid=2, specialize=img)
+        text = open(os.path.join(P.KERNELS, "b200", form + ".mk")).read()
+        if block and form == "ethash":
+            text = text.replace("dims (1024, 1, 1)", f"dims ({block}, 1, 1)")
+        m = hf.Module.kernel(text, grid=2, specialize=img)
         print(form, m.entry, "regs", m.info.regs, flush=True)
         m.run(img, 2)
         n += 1
@@ -52,7 +58,9 @@ for a, b, d2, regs in [("sha256d", "blake2b", 512, (40, 56)), ("blake256", "etha
     n += 2
 # Ethash alone in both forms (the lean member parks seeds in shared memory across warp_sync and
 # stages DAG pages through cp.async; 1,024 threads at 2 blocks)
-we = CR.workload("ethash", 64, 2, nonce0=3, target=1 << 28)  # racecheck instruments every shared access: keep it small
+# 4,096 nonces: every warp of both blocks walks (at 64 nonces only 2 of 32 warps would; see
+# profiles/r02_racecheck_ethash_shapes.log for that degenerate shape)
+we = CR.workload("ethash", 4096, 2, nonce0=3, target=1 << 28)
 img = hf.Image(we.image).upload()
 for form in ([] if sys.argv[1:] == ["no-ethash"] else CR.FORMS["ethash"]):
     hf.Module.kernel(open(os.path.join(P.KERNELS, "b200", form + ".mk")).read(), grid=2, specialize=img).run(img, 2)

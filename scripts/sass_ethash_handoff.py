@@ -1,9 +1,9 @@
-"""SASS evidence for the lean Ethash seed hand-off (profiles/r02_ethash_seed_handoff_sass.txt): the
-8-lane groups exchange Keccak-512 seeds through shared memory, ordered in the source by MK+
-warp_sync (__syncwarp). ptxas proves the warp converged there and emits no WARPSYNC between the
-STS of the seeds and the LDS of the partners' words (the warp's shared accesses then execute in
-program order), which compute-sanitizer racecheck, seeing no barrier event, reports as a hazard
-(profiles/r02_racecheck_ethash_forms.log). Runs on the CPU (NVRTC source + nvcc -cubin).
+"""SASS of the lean Ethash seed hand-off (profiles/r02_ethash_seed_handoff_sass.txt): the 8-lane
+groups exchange Keccak-512 seeds through shared memory, ordered in the source by MK+ warp_sync
+(__syncwarp). ptxas compiles that sync to a divergence check (BRA.DIV) with no WARPSYNC on the
+converged path between the seed STS and the partners' LDS. Context for the one racecheck report on
+a degenerate launch shape (profiles/r02_racecheck_ethash_shapes.log). Runs on the CPU (NVRTC
+source + nvcc -cubin).
 python scripts/sass_ethash_handoff.py"""
 import os
 import re
@@ -33,7 +33,7 @@ first_sts = next(i for i, l in enumerate(ins) if "STS" in l)
 first_lds = next(i for i, l in enumerate(ins) if "LDS" in l and i > first_sts)
 window = ins[first_sts:first_lds + 12]
 between = ins[first_sts:first_lds]
-out = [__doc__.split("\n\n")[0], "",
+out = [__doc__.split("\npython")[0], "",
        f"source: __syncwarp() at line {sync_line} of the specialized ethash source (grid 2, 1,024 threads)",
        f"WARPSYNC between the first seed STS and the first partner LDS: {any('WARPSYNC' in l for l in between)}",
        f"WARPSYNC anywhere in the kernel: {sum('WARPSYNC' in l for l in ins)} (warp_bcast's partial-warp path)", ""]
