@@ -183,3 +183,34 @@ def test_sha256d_blake2b_fused_at_scale(gpu):
     img.download()
     assert device_outputs(img, "sha256d") == reference_outputs("sha256d", n, grid, 123, 1 << 20)
     assert device_outputs(img, "blake2b") == reference_outputs("blake2b", n, grid, 456, 1 << 20)
+
+
+PIPE_VARIANTS = [("sha256d", {"HF_SHA_ADDS": "fma"}), ("blake256", {"HF_B256_ADDS": "a"}),
+                 ("blake256", {"HF_B256_ADDS": "ac"})]
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+@pytest.mark.parametrize("kind,env", PIPE_VARIANTS)
+def test_fma_add_generator_variants_on_reference_interpreter(hf, kind, env, tmp_path, monkeypatch):
+    """The generator's pipe-balance variants (adds as MK+ fma_add, profiles/r02_probe_hash_adds.jsonl)
+    compute the same hash: lowered, they reproduce the restatement on the reference interpreter."""
+    import importlib
+    from paper_2007_01277_b200.kernels import gen_crypto
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = importlib.reload(gen_crypto)
+    try:
+        text = {"sha256d": g.gen_sha256d, "blake256": g.gen_blake256}[kind]()
+    finally:
+        monkeypatch.undo()
+        importlib.reload(gen_crypto)
+    assert "fma_add(" in text
+    count, grid, nonce0, target = 40, 1, 1000, 1 << 31
+    w = crypto.workload(kind, count=count, grid=grid, nonce0=nonce0, target=target)
+    (tmp_path / "k.mk").write_text(hf.lower(text))
+    (tmp_path / "k.img").write_text(w.image)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img", "--grid", grid)
+    arrays, _ = oracle.parse_image(dump)
+    p = crypto.MEMBERS[kind]
+    want = reference_outputs(kind, count, grid, nonce0, target)
+    assert int(arrays[f"{p}_chk"][0]) == want["chk"] and int(arrays[f"{p}_cnt"][0]) == want["cnt"]
