@@ -72,6 +72,10 @@ ETHASH_TMAX = 512  # async form: the shared ring is sized for intervals of up to
 # baselines run whichever form is faster, so a fused win is never a win over a slowed member.
 ETHASH_FORM = os.environ.get("HF_ETHASH_FORM", "lean")
 ETHASH_LEAN_TMAX = int(os.environ.get("HF_ETHASH_TMAX", "1024"))
+# Keccak-f as 24 straight-line rounds with immediate round constants (HF_KECCAK_UNROLL=1) instead
+# of a rolled round loop reading the constants from eh_rc (probe: register pressure / spills of the
+# lean Ethash member at 64 registers)
+KECCAK_UNROLL = os.environ.get("HF_KECCAK_UNROLL", "") == "1"
 ROT = [[0, 36, 3, 41, 18], [1, 44, 10, 45, 2], [62, 6, 43, 15, 61], [28, 55, 25, 21, 56], [27, 20, 39, 8, 14]]
 
 
@@ -505,8 +509,18 @@ def keccak_f(src, A, rc_array):
     round constants come from rc_array (48 words)."""
     C = [Lane(f"c{x}l", f"c{x}h") for x in range(5)]
     D = Lane("dl", "dh")
+    if KECCAK_UNROLL:
+        for r in range(24):
+            _keccak_round(src, A, C, D, hx(RC[r]), hx(RC[r] >> 32))
+        return
     src("for (int rnd = 0; rnd < 24; rnd = rnd + 1) {")
     src.ind += 1
+    _keccak_round(src, A, C, D, f"{rc_array}[rnd * 2]", f"{rc_array}[rnd * 2 + 1]")
+    src.ind -= 1
+    src("}")
+
+
+def _keccak_round(src, A, C, D, rc_lo, rc_hi):
     for x in range(5):
         for half in ("lo", "hi"):
             terms = " ^ ".join(getattr(A[(x, y)], half) for y in range(5))
@@ -541,10 +555,10 @@ def keccak_f(src, A, rc_array):
             b1, b2 = C[(x + 1) % 5], C[(x + 2) % 5]
             src(f"{A[(x, y)].lo} = {C[x].lo} ^ (({b1.lo} ^ -1) & {b2.lo});")
             src(f"{A[(x, y)].hi} = {C[x].hi} ^ (({b1.hi} ^ -1) & {b2.hi});")
-    src(f"{A[(0, 0)].lo} = {A[(0, 0)].lo} ^ {rc_array}[rnd * 2];")
-    src(f"{A[(0, 0)].hi} = {A[(0, 0)].hi} ^ {rc_array}[rnd * 2 + 1];")
-    src.ind -= 1
-    src("}")
+    if rc_lo != "0x00000000":
+        src(f"{A[(0, 0)].lo} = {A[(0, 0)].lo} ^ {rc_lo};")
+    if rc_hi != "0x00000000":
+        src(f"{A[(0, 0)].hi} = {A[(0, 0)].hi} ^ {rc_hi};")
 
 
 def absorb_words(src, A, words):
