@@ -214,3 +214,40 @@ def test_fma_add_generator_variants_on_reference_interpreter(hf, kind, env, tmp_
     p = crypto.MEMBERS[kind]
     want = reference_outputs(kind, count, grid, nonce0, target)
     assert int(arrays[f"{p}_chk"][0]) == want["chk"] and int(arrays[f"{p}_cnt"][0]) == want["cnt"]
+
+
+WRAP = [(0x7FFFFFE0, 40), (-24, 40)]  # across 2^31 (signed overflow) and across 2^32 -> 0
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference build (oracle/_ref) not present")
+@pytest.mark.parametrize("nonce0,count", WRAP)
+@pytest.mark.parametrize("kind", ["sha256d", "blake256", "blake2b"])
+def test_nonce_range_wrap_on_reference_interpreter(hf, kind, nonce0, count, tmp_path):
+    """Nonce ranges that cross 2^31 (the int32 nonce turns negative) and 2^32 (wraps to 0): the
+    lowered member on the reference interpreter equals the restatement, per-block minimum included
+    (a hit below 0x7fffffff after the wrap is a smaller signed value than one before it)."""
+    grid, target = 1, 1 << 31
+    w = crypto.workload(kind, count=count, grid=grid, nonce0=nonce0, target=target)
+    (tmp_path / "k.mk").write_text(hf.lower(src(kind)))
+    (tmp_path / "k.img").write_text(w.image)
+    _, _, dump = oracle.ref_run("run", tmp_path / "k.mk", "--mem", tmp_path / "k.img", "--grid", grid)
+    arrays, _ = oracle.parse_image(dump)
+    p = crypto.MEMBERS[kind]
+    want = reference_outputs(kind, count, grid, nonce0, target)
+    assert int(arrays[f"{p}_cnt"][0]) == want["cnt"] and int(arrays[f"{p}_chk"][0]) == want["chk"]
+    assert [int(x) for x in arrays[f"{p}_bmin"]] == want["bmin"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nonce0", [0x7FFFFF00, -700])
+@pytest.mark.parametrize("kind,form", FORMS)
+def test_nonce_range_wrap_on_device(gpu, kind, form, nonce0):
+    """The same wraps on the B200 with a ragged count (not a multiple of the block) over 3 blocks."""
+    hf = gpu
+    count, grid, target = (1300 if kind == "ethash" else 3001), 3, 1 << 28
+    w = crypto.workload(kind, count=count, grid=grid, nonce0=nonce0, target=target)
+    img = hf.Image(w.image).upload()
+    hf.Module.kernel(src(form), grid=grid, specialize=img).run(img, grid)
+    img.download()
+    thr = crypto.FORM_THREADS.get(form, crypto.THREADS[kind])
+    assert device_outputs(img, kind) == reference_outputs(kind, count, grid, nonce0, target, threads=thr)
