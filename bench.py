@@ -667,8 +667,9 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         D.barrier()
-        with torch.cuda.stream(stream):
-            torch.cuda._sleep(spin_cycles)
+        if hasattr(torch.cuda, "_sleep"):  # private torch API: without it the region is just not pre-queued
+            with torch.cuda.stream(stream):
+                torch.cuda._sleep(spin_cycles)
         e0.record(stream)
         for s in range(args.steps):
             fn(s)
