@@ -104,28 +104,6 @@ def reduce_gathered(layout: Layout, gathered, bn_counts):
     return out
 
 
-def reduce_outputs(dist, hist_bins=None, bn_stats=None, bn_count=None):
-    """Single-pair convenience form: hist_bins int32 [64] (reduced in place), bn_stats float32
-    [2C] (mean, var) of this rank's shard -> merged (mean, var) as float64 numpy arrays."""
-    import torch
-    layout = Layout()
-    parts = []
-    if hist_bins is not None:
-        layout.add("hist", "hist", hist_bins.numel())
-        parts.append(hist_bins.to(torch.int32).reshape(-1))
-    if bn_stats is not None:
-        layout.add("bn", "bn", bn_stats.numel(), bn_stats.numel() // 2)
-        parts.append(bn_stats.to(torch.float32).reshape(-1).view(torch.int32))
-    gathered = all_gather_packed(dist, torch.cat(parts))
-    red = reduce_gathered(layout, gathered, [bn_count] * dist.get_world_size())
-    if hist_bins is not None:
-        hist_bins.copy_(red["hist"].to(hist_bins.dtype))
-    if bn_stats is None:
-        return None
-    m, v = red["bn"]
-    return m.cpu().numpy(), v.cpu().numpy()
-
-
 def nonce_slice(total: int, rank: int, world: int) -> Tuple[int, int]:
     """(nonce0, count) of rank's contiguous slice of [0, total)."""
     if total % world:
