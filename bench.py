@@ -610,16 +610,14 @@ def main():
     if "bn" in keys:
         bn_count = [int(P.shard("bn", shape, r, sworld).image.split("scalar bn_N int32 ")[1].split()[0]) *
                     int(work["bn"].image.split("scalar bn_HW int32 ")[1].split()[0]) for r in range(world)]
-    import ctypes
-    _cudart = ctypes.CDLL("libcudart.so.12")
     src_ptr = [(imgs[i].device_ptr(name), off, cells) for i, name, off, cells in copies]
     merged = {}
 
     def reduce_step():
-        for ptr, off, cells in src_ptr:  # device-to-device gather of the outputs into one buffer
-            _cudart.cudaMemcpyAsync(ctypes.c_void_p(packed.data_ptr() + 4 * off), ctypes.c_void_p(ptr),
-                                    ctypes.c_size_t(4 * cells), 3, ctypes.c_void_p(stream.cuda_stream))
-        merged["out"] = SH.reduce_gathered(layout, D.gather(packed), bn_count)
+        # three launches per step: pack the outputs into one buffer, all-gather it, reduce it
+        # (csrc/shard_reduce.cu; shard.reduce_gathered is the torch restatement it is tested against)
+        hf.shard_pack(src_ptr, packed.data_ptr(), stream.cuda_stream)
+        merged["out"] = SH.reduce_gathered_device(hf, layout, D.gather(packed), bn_count)
 
     dist_on = world > 1
 

@@ -309,6 +309,30 @@ int hf_search(const char* src1, const char* src2, hf_image* img, hf_search_opts*
               int* best_d1, int* best_d2, int* best_regcap, long long* best_time,
               char** trace_csv, char** best_src, hf_error* err);
 
+/* The multi-GPU step exchange on the device (B200-only; the reference is single-threaded,
+ * /root/reference/SPEC.md:374). Each rank packs its step outputs into one int32 buffer
+ * (hf_shard_pack: one launch for up to 32 source arrays), the buffers are all-gathered (NCCL),
+ * and hf_shard_reduce reduces the [world, cells] result in one launch: hist slots -> int64 sums,
+ * bn slots -> Chan's merge of (mean, biased var) in rank order in fp64 without contraction
+ * (mean[C] then var[C]), crypto slots -> int64 (hit sum, winning-nonce min) pairs. `out` holds
+ * 8-byte elements at each slot's out_offset; counts = per-rank elements per channel (bn). */
+enum { HF_SLOT_HIST = 0, HF_SLOT_BN = 1, HF_SLOT_CRYPTO = 2 };
+typedef struct hf_pack_src {
+  const void* src;
+  long long offset;
+  long long cells;
+} hf_pack_src;
+typedef struct hf_reduce_slot {
+  int kind;
+  int channels;
+  long long offset;
+  long long cells;
+  long long out_offset;
+} hf_reduce_slot;
+int hf_shard_pack(const hf_pack_src* srcs, int n, int* packed, void* stream, hf_error* err);
+int hf_shard_reduce(const int* gathered, int world, long long cells, const hf_reduce_slot* slots,
+                    int nslots, const double* counts, void* out, void* stream, hf_error* err);
+
 #ifdef __cplusplus
 }
 #endif

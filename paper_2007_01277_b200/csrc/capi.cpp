@@ -11,6 +11,7 @@
 #include "driver.hpp"
 #include "runtime.hpp"
 #include "search.hpp"
+#include "shard_reduce.hpp"
 
 struct hf_module {
   hf::rt::Module m;
@@ -466,6 +467,23 @@ int hf_time(int mode, const hf_module* a, const hf_module* b, hf_image* img, int
     hf::rt::Timing t = hf::rt::time(md, a->m, b ? &b->m : nullptr, img->img, grid_a, grid_b, warmup, reps,
                                     flush_l2 != 0, stream);
     *out = hf_timing{t.median_us, t.min_us, t.mean_us, t.max_us, t.reps, t.iqm_us};
+  });
+}
+
+static_assert(sizeof(hf_pack_src) == sizeof(hf::shard::PackSrc), "hf_pack_src layout");
+static_assert(sizeof(hf_reduce_slot) == sizeof(hf::shard::ReduceSlot), "hf_reduce_slot layout");
+
+int hf_shard_pack(const hf_pack_src* srcs, int n, int* packed, void* stream, hf_error* err) {
+  return guarded(err, [&] {
+    hf::shard::pack(reinterpret_cast<const hf::shard::PackSrc*>(srcs), n, packed, stream);
+  });
+}
+
+int hf_shard_reduce(const int* gathered, int world, long long cells, const hf_reduce_slot* slots, int nslots,
+                    const double* counts, void* out, void* stream, hf_error* err) {
+  return guarded(err, [&] {
+    hf::shard::reduce(gathered, world, cells, reinterpret_cast<const hf::shard::ReduceSlot*>(slots), nslots, counts,
+                      out, stream);
   });
 }
 

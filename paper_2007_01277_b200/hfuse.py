@@ -45,8 +45,10 @@ EXPORTS = [
     "hf_image_materialize", "hf_image_upload", "hf_image_download", "hf_image_digest",
     "hf_image_serialize", "hf_image_count", "hf_image_entry", "hf_image_find",
     "hf_image_set_host", "hf_image_bytes", "hf_image_free", "hf_run", "hf_time", "hf_time_graph", "hf_profile",
-    "hf_search",
+    "hf_search", "hf_shard_pack", "hf_shard_reduce",
 ]
+
+SLOT_KINDS = {"hist": 0, "bn": 1, "crypto": 2}
 
 
 class HFuseError(Exception):
@@ -106,6 +108,15 @@ class _SearchOpts(C.Structure):
                 ("out_style", C.c_int), ("interval_regs", C.c_int), ("budget_points", C.c_int),
                 ("best_regs1", C.c_int), ("best_regs2", C.c_int), ("prefilter", C.c_int),
                 ("prefilter_tol", C.c_double), ("model_csv", C.c_void_p)]
+
+
+class _PackSrc(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("offset", C.c_longlong), ("cells", C.c_longlong)]
+
+
+class _ReduceSlot(C.Structure):
+    _fields_ = [("kind", C.c_int), ("channels", C.c_int), ("offset", C.c_longlong), ("cells", C.c_longlong),
+                ("out_offset", C.c_longlong)]
 
 
 class _Props(C.Structure):
@@ -172,6 +183,9 @@ def _load() -> C.CDLL:
         "hf_time": (ip, [ip, vp, vp, vp, ip, ip, ip, ip, ip, vp, C.POINTER(_Timing), E]),
         "hf_time_graph": (ip, [ip, vp, vp, vp, ip, ip, ip, ip, vp, C.POINTER(_GraphTiming), E]),
         "hf_profile": (ip, [cp, cp, ip, ip, ip, vp, ip, ip, ip, ip, ip, C.POINTER(_Eval), E]),
+        "hf_shard_pack": (ip, [C.POINTER(_PackSrc), ip, vp, vp, E]),
+        "hf_shard_reduce": (ip, [vp, ip, C.c_longlong, C.POINTER(_ReduceSlot), ip, C.POINTER(C.c_double), vp, vp,
+                                 E]),
         "hf_search": (ip, [cp, cp, vp, C.POINTER(_SearchOpts), C.POINTER(ip), C.POINTER(ip), C.POINTER(ip),
                            C.POINTER(C.c_longlong), C.POINTER(vp), C.POINTER(vp), E]),
     }
@@ -572,6 +586,26 @@ def time(mode: str, a: Module, b: Optional[Module], img: Image, grid_a: int = 0,
                         int(flush_l2), _stream(stream), C.byref(t), C.byref(err)), err)
     return {"median_us": t.median_us, "min_us": t.min_us, "mean_us": t.mean_us, "max_us": t.max_us,
             "reps": t.reps, "iqm_us": t.iqm_us}
+
+
+def shard_pack(sources, packed_ptr: int, stream=None) -> None:
+    """One launch copying int32 device arrays into a packed buffer: sources = [(device pointer,
+    cell offset, cells)] (the multi-GPU step's send buffer, include/hfuse.h hf_shard_pack)."""
+    arr = (_PackSrc * max(1, len(sources)))(*[_PackSrc(p, o, n) for p, o, n in sources])
+    err = _Err()
+    _check(_lib.hf_shard_pack(arr, len(sources), C.c_void_p(packed_ptr), _stream(stream), C.byref(err)), err)
+
+
+def shard_reduce(gathered_ptr: int, world: int, cells: int, slots, counts, out_ptr: int, stream=None) -> None:
+    """One launch reducing an all-gathered [world, cells] int32 buffer: slots = [(kind, channels,
+    cell offset, cells, out offset in 8-byte elements)], kind in SLOT_KINDS; counts = per-rank
+    elements per channel for bn slots (include/hfuse.h hf_shard_reduce)."""
+    arr = (_ReduceSlot * max(1, len(slots)))(*[_ReduceSlot(SLOT_KINDS.get(k, k), ch, o, n, oo)
+                                                for k, ch, o, n, oo in slots])
+    cnt = (C.c_double * max(1, len(counts or [])))(*(counts or [0.0]))
+    err = _Err()
+    _check(_lib.hf_shard_reduce(C.c_void_p(gathered_ptr), world, cells, arr, len(slots), cnt if counts else None,
+                                C.c_void_p(out_ptr), _stream(stream), C.byref(err)), err)
 
 
 def time_graph(mode: str, a: Module, b: Optional[Module], img: Image, grid_a: int = 0, grid_b: int = 0,

@@ -54,7 +54,9 @@ def merge_bn_torch(counts, means, variances):
         mean = mean + delta * (c / tot)
         m2 = m2 + variances[r] * c + delta * delta * (n * c / tot)
         n = tot
-    return mean, m2 / n
+    # a true division (torch turns division by a Python scalar into a reciprocal multiply, which
+    # rounds differently from merge_bn_stats and the device merge)
+    return mean, m2 / torch.tensor(n, dtype=torch.float64, device=m2.device)
 
 
 @dataclass
@@ -97,11 +99,42 @@ def reduce_gathered(layout: Layout, gathered, bn_counts):
             st = block.contiguous().view(torch.float32).reshape(block.shape[0], ch, 2)
             out[tag] = merge_bn_torch(bn_counts, st[:, :, 0], st[:, :, 1])
         elif kind == "crypto":  # (hits, winning nonce) pairs as int64 = 2 int32 cells each
-            v = block.contiguous().view(torch.int64).reshape(block.shape[0], -1, 2)
+            # a flat copy: offset 0 and an even length whatever the slot's offset and the row stride
+            v = block.reshape(-1).clone().view(torch.int64).reshape(block.shape[0], -1, 2)
             out[tag] = (v[:, :, 0].sum(0), v[:, :, 1].min(0).values)
         else:
             raise ValueError(kind)
     return out
+
+
+def reduce_gathered_device(hf, layout: Layout, gathered, bn_counts):
+    """reduce_gathered in ONE kernel launch (hf.shard_reduce, csrc/shard_reduce.cu) for a CUDA
+    [world, cells] int32 buffer: the same dict, bit-identical (the kernel's fp64 Chan merge keeps
+    merge_bn_torch's operation order with no contraction; tests/test_shard_reduce_gpu.py)."""
+    import torch
+    slots, views, o = [], [], 0
+    for kind, tag, off, cells, ch in layout.slots:
+        n = {"hist": cells, "bn": 2 * ch, "crypto": cells // 2}[kind]
+        slots.append((kind, ch, off, cells, o))
+        views.append((kind, tag, o, n, ch))
+        o += n
+    out = torch.empty(max(1, o), dtype=torch.int64, device=gathered.device)
+    g = gathered.contiguous()
+    counts = [float(c) for c in bn_counts] if bn_counts is not None else None
+    hf.shard_reduce(g.data_ptr(), g.shape[0], g.shape[1], slots, counts, out.data_ptr(),
+                    torch.cuda.current_stream(g.device).cuda_stream)
+    res = {}
+    for kind, tag, o, n, ch in views:
+        block = out[o:o + n]
+        if kind == "hist":
+            res[tag] = block
+        elif kind == "bn":
+            f = block.view(torch.float64)
+            res[tag] = (f[:ch], f[ch:])
+        else:
+            p = block.reshape(-1, 2)
+            res[tag] = (p[:, 0], p[:, 1])
+    return res
 
 
 def nonce_slice(total: int, rank: int, world: int) -> Tuple[int, int]:

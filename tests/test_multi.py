@@ -129,3 +129,18 @@ def test_nonce_slices_cover_the_range():
         sl = [shard.nonce_slice(1 << 20, r, world) for r in range(world)]
         assert sl[0][0] == 0 and all(a[0] + a[1] == b[0] for a, b in zip(sl, sl[1:]))
         assert sum(c for _, c in sl) == 1 << 20
+
+
+def test_torch_merge_is_bit_identical_to_the_numpy_merge():
+    """merge_bn_torch (the bench's reduction restated in torch, and the reference the device merge
+    in csrc/shard_reduce.cu is tested against bit for bit) equals merge_bn_stats exactly."""
+    import torch
+    from paper_2007_01277_b200 import shard as SH
+    rng = np.random.default_rng(3)
+    for world in (1, 2, 5, 8):
+        means = rng.normal(0, 1, (world, 256)).astype(np.float32)
+        vars_ = rng.uniform(0.1, 2, (world, 256)).astype(np.float32)
+        counts = [int(c) for c in rng.integers(1000, 9000, world)]
+        m, v = SH.merge_bn_stats(counts, list(means), list(vars_))
+        tm, tv = SH.merge_bn_torch(counts, torch.tensor(means), torch.tensor(vars_))
+        assert np.array_equal(tm.numpy(), m) and np.array_equal(tv.numpy(), v)
