@@ -866,7 +866,8 @@ def main():
                      **({"traffic_config": traffic_cfg} if traffic_cfg else {})},
         "e2e": {"value": round(e2e["value"], 1), "unit": "us", "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
                 "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]},
-        "gpu_launches": len(pair_list) * args.steps,
+        # the ten fused kernels per step, plus the exchange's pack and reduce kernels when N > 1
+        "gpu_launches": (len(pair_list) + (2 if dist_on else 0)) * args.steps,
         "clocks": {k: clk.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         "cpu_baseline": cpu,
     }
