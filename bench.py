@@ -370,7 +370,7 @@ def fused_grids(d0, waves):
     return [resident * w for w in waves]
 
 
-def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3, natural=0):
+def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=6, natural=0):
     """Device split search over block size d0 x launch grid (search_config per grid, steady
     graph protocol), then the `top` fastest distinct points re-timed with a longer graph (the
     minimum of a few hundred short samples is biased low; the re-timing picks on equal terms).
@@ -388,6 +388,8 @@ def search_pair(hf, sa, sb, img, d0s, grids, stream, args, top=3, natural=0):
     best = None
     # the `top` fastest screened points of each family (static split, heterogeneous partition)
     # re-timed on equal terms: a screen's noise must not hand one family all the final slots
+    # (BN + Hist screens dozens of points within 0.05 us of each other, so three finalists were a
+    # lottery between 59.8 and 61.0 us across runs)
     finalists = []
     for fam in (False, True):
         finalists += sorted((c for c in cands if bool(c[0]["split_grid"]) == fam), key=lambda c: c[1])[:top]
