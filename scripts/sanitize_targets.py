@@ -4,7 +4,7 @@ synccheck): named-barrier rewriting must not introduce shared-memory races or ba
 Covers: corpus pairs (reference Mini-Kernel), the ten DL pairs (B200 forms, parity sizes, two
 splits), the crypto pairs (one register cap and per-interval budgets), the hand-off BatchNorm,
 a CUDA-frontend pair, and (round 2) dynamic interval scheduling (block- and warp-level queues,
-two launches each) and an MK+ async_copy kernel."""
+two launches each), an MK+ async_copy kernel and the multi-GPU exchange's pack and reduce kernels."""
 import os
 import sys
 
@@ -87,6 +87,18 @@ import test_async_copy as TA  # noqa: E402
 img = hf.Image(TA.IMG).upload()
 hf.Module.kernel(TA.SRC).run(img)
 n += 1
+# the multi-GPU step exchange kernels (csrc/shard_reduce.cu): pack + reduce over an odd-length
+# layout at world 8 (int64 words at odd cell offsets)
+import test_shard_reduce_gpu as TS  # noqa: E402
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from paper_2007_01277_b200 import shard as SH  # noqa: E402
+lay, g, counts = TS.layout_and_data(torch, 8, np.random.default_rng(8))
+SH.reduce_gathered_device(hf, lay, g, counts)
+srcs = [torch.arange(k, dtype=torch.int32, device="cuda") for k in (64, 63, 1)]
+packed = torch.zeros(200, dtype=torch.int32, device="cuda")
+hf.shard_pack([(t.data_ptr(), o, t.numel()) for t, o in zip(srcs, (0, 70, 140))], packed.data_ptr())
+n += 2
 import ctypes  # noqa: E402
 assert ctypes.CDLL("libcudart.so.12").cudaDeviceSynchronize() == 0
 print(f"sanitize targets: {n} fused launches")
